@@ -1,0 +1,151 @@
+/*
+ * codegemm_b200.h -- C ABI of the B200-native CodeGEMM decode path.
+ *
+ * Plain pointers and sizes only (no torch / CUDA runtime types in the
+ * signatures: streams are passed as `void*` holding a cudaStream_t, NULL =
+ * the legacy default stream).  The library is libcodegemm_b200.so, built for
+ * sm_100a only; there is no CPU fallback -- every compute entry point fails
+ * with CG_ERR_CUDA when no B200 is present.
+ *
+ * Each entry point replaces one piece of the reference's Python operator
+ * path (/root/reference/pkg/src/codegemm/...):
+ *
+ *   cg_layer_create       QuantizedLayer as the engines consume it:
+ *                         CodePlane (quantizer.py:135-145), Codebook
+ *                         (quantizer.py:87-113), ScalePlane (quantizer.py:116-132),
+ *                         segment_groups (quantizer.py:195-199).  Uploads and
+ *                         prepacks the planes once (weights are static).
+ *   cg_layer_gemm         codegemm_gemm(q, x, tiles, threads) (engines.py:245-316)
+ *                         on device buffers; CG_MODE_STRICT reproduces its
+ *                         binary32 operation order bit for bit (engines.py:15-22),
+ *                         CG_MODE_FAST is the fused lookup kernel (tolerance parity).
+ *   cg_layer_gemm_host    the same call with HOST buffers (the drop-in used by
+ *                         the Python shim: x in, y out, copies included).
+ *   cg_layer_psumbook     the fused kernel's on-chip Psumbook, dumped in the layout
+ *                         of _psum_tables (engines.py:115-134) for bit-exact checks.
+ *   cg_psumbook_build     standalone Psumbook build, build_psumbook / _psum_tables
+ *                         (engines.py:115-156).
+ *   cg_layer_unpack_codes inverse of the device prepack; returns the per-row gather
+ *                         indices as uint16 planes (CodePlane.codes) for bit-exact
+ *                         index parity (pack/unpack: quantizer.py:471-497).
+ *
+ * Errors: every int-returning function returns CG_OK (0) or a CG_ERR_* code
+ * and records a message retrievable with cg_last_error() (thread-local).  The
+ * codes map onto the reference exception classes (errors.py:4-37):
+ * CG_ERR_CONFIG -> ConfigError, CG_ERR_SHAPE -> ShapeError,
+ * CG_ERR_INTEGRITY -> IntegrityError.
+ *
+ * Threading: functions are reentrant across layers and streams; one layer
+ * handle owns a split-K workspace, so calls on the SAME handle must be
+ * ordered on one stream (or serialised by the caller).
+ */
+#ifndef CODEGEMM_B200_H
+#define CODEGEMM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CG_ABI_VERSION 1
+
+#define CG_OK 0
+#define CG_ERR_CONFIG 1      /* bad hyper-parameters / tiling       -> ConfigError    */
+#define CG_ERR_SHAPE 2       /* inconsistent operand shapes         -> ShapeError     */
+#define CG_ERR_INTEGRITY 3   /* invalid layer contents (code range) -> IntegrityError */
+#define CG_ERR_CUDA 4        /* CUDA runtime / launch failure, no device              */
+#define CG_ERR_UNSUPPORTED 5 /* config outside the requested mode's kernels           */
+#define CG_ERR_ARG 6         /* NULL / out-of-range argument                          */
+
+#define CG_MODE_AUTO 0   /* FAST when the config has a fused kernel, else STRICT      */
+#define CG_MODE_FAST 1   /* fused Psumbook + code-gather kernel (fp32 accumulate)      */
+#define CG_MODE_STRICT 2 /* reference operation order: bit-identical to codegemm_gemm  */
+
+/* option flags for cg_layer_options.flags */
+#define CG_OPT_NO_PDL 1        /* launch without programmatic dependent launch        */
+#define CG_OPT_NO_L2_PREFETCH 2 /* skip the bulk L2 prefetch of the CTA's code tiles   */
+
+typedef struct cg_layer cg_layer;
+
+typedef struct cg_layer_options {
+    int u;             /* segments per lane per K-slice (1, 2, 4); 0 = planner choice */
+    int rg_per_task;   /* 16-row groups per CTA task; 0 = planner choice              */
+    int flags;         /* CG_OPT_*                                                     */
+    int device;        /* CUDA device ordinal; -1 = current device                    */
+} cg_layer_options;
+
+typedef struct cg_layer_info {
+    int64_t rows, cols;
+    int v, m, b;
+    int64_t g;              /* as given (-1 = one scale per row)                       */
+    int fast_supported;     /* 1 if CG_MODE_FAST has a kernel for this config           */
+    int u;                  /* chosen segments-per-lane                                */
+    int rg_per_task;        /* chosen 16-row groups per CTA task                       */
+    int64_t n_slices;       /* K-slices of 32*u segments                               */
+    int64_t n_tasks;        /* CTAs of the fused kernel                                */
+    int smem_bytes;         /* dynamic shared memory of the fused kernel                */
+    int launches_fast;      /* kernels one CG_MODE_FAST call launches (1 or 2)         */
+    int64_t device_bytes;   /* device memory owned by the handle                       */
+    int64_t algorithmic_bytes; /* codes (b bits) + scales + codebooks for one call,
+                                   excluding x and y                    */
+} cg_layer_info;
+
+int cg_abi_version(void);
+const char* cg_last_error(void);
+
+/* Number of CUDA devices visible (0 when none); never fails. */
+int cg_device_count(void);
+
+/*
+ * Create a device-resident layer from HOST arrays in the reference layout.
+ *   codes[t]  : (rows, cols/v) uint16, row-major, t < m    (CodePlane.codes)
+ *   books[t]  : (2**b, v) binary16 bit patterns           (Codebook.entries)
+ *   scales    : (rows, cols/g_eff) binary16 bit patterns  (ScalePlane.scales)
+ *   g         : group size, -1 = one scale per row
+ * A row shard is created by passing row-offset pointers and the shard's rows.
+ * opts may be NULL (planner defaults).
+ */
+int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
+                    const uint16_t* scales, int64_t rows, int64_t cols, int v, int m, int b,
+                    int64_t g, const cg_layer_options* opts, cg_layer** out);
+int cg_layer_destroy(cg_layer* layer);
+int cg_layer_query(const cg_layer* layer, cg_layer_info* info);
+
+/*
+ * y = W x on device buffers, stream-ordered, asynchronous.
+ *   x : (cols, n) binary16, row-major (Matrix layout: one column per token)
+ *   y : (rows, n) float32, row-major
+ */
+int cg_layer_gemm(cg_layer* layer, const void* x, int n, float* y, int mode, void* stream);
+
+/* Same with HOST buffers: copies x in, runs, copies y out, synchronises. */
+int cg_layer_gemm_host(cg_layer* layer, const uint16_t* x, int n, float* y, int mode,
+                       void* stream);
+
+/*
+ * Psumbook of the fused kernel for input x (device (cols, n) binary16), written
+ * to out (device float32, (m, cols/v, 2**b, n) -- _psum_tables layout).
+ * Requires fast_supported.
+ */
+int cg_layer_psumbook(cg_layer* layer, const void* x, int n, float* out, void* stream);
+
+/*
+ * Per-row gather indices recovered from the prepacked device layout:
+ * out (device uint16, (m, rows, cols/v)).
+ */
+int cg_layer_unpack_codes(cg_layer* layer, uint16_t* out, void* stream);
+
+/*
+ * Standalone Psumbook build on device buffers:
+ *   books : m x (2**b, v) binary16 contiguous;  x : (k_len, n) binary16
+ *   out   : (m, k_len/v, 2**b, n) float32
+ */
+int cg_psumbook_build(const void* books, const void* x, int m, int b, int v, int64_t k_len,
+                      int n, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CODEGEMM_B200_H */

@@ -1,0 +1,499 @@
+// cg_api.cu -- extern "C" entry points of libcodegemm_b200.so (include/codegemm_b200.h).
+//
+// The layer handle owns the device-resident prepacked weights (uploaded once,
+// weights are static), a split-K workspace and pinned staging buffers for the
+// host-buffer entry point.  Validation mirrors the reference exactly:
+//   QuantConfig / validate_shape  (quantizer.py:35-84)      -> CG_ERR_CONFIG
+//   code range                    (quantizer.py:181-182)    -> CG_ERR_INTEGRITY
+//   q.cols != x.rows              (engines.py:184-186)      -> CG_ERR_SHAPE (n < 1 here)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/codegemm_b200.h"
+#include "cg_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(CG_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define CG_CUDA(call, what)                                 \
+    do {                                                    \
+        cudaError_t _e = (call);                            \
+        if (_e != cudaSuccess) return cuda_fail(_e, what);  \
+    } while (0)
+
+int sm_count_of(int device) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n < 1)
+        return 148;
+    return n;
+}
+
+bool pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+
+int ilog2(int64_t x) {
+    int r = 0;
+    while ((1LL << r) < x) ++r;
+    return r;
+}
+
+// Scale-group constraint of the fused kernel for segments-per-lane u: returns
+// lg = log2(lanes sharing one scale group) or -1 when a lane's u segments
+// would straddle groups / slices would straddle groups.
+int scale_lg(const cg::Plan& p, int u) {
+    if (p.g_row) return 5;
+    const int64_t lane_elems = (int64_t)u * p.v, slice_elems = 32 * lane_elems;
+    if (p.g_eff >= slice_elems) return (p.g_eff % slice_elems == 0) ? 5 : -1;
+    if (p.g_eff % lane_elems != 0 || slice_elems % p.g_eff != 0) return -1;
+    const int64_t lanes = p.g_eff / lane_elems;
+    if (!pow2(lanes)) return -1;
+    return ilog2(lanes);
+}
+
+// Planner: pick u (segments per lane) and rows per task for the fused kernel.
+// Cost model per SM, in shared-memory wavefronts (the co-bound with HBM):
+//   gather  = rows/16 * 16*(u*m + 1)   (one LDS per lookup + SHFL reduction)
+//   build   = m*u*2**kb                (STS.128 of the slice tables)
+// with tasks = n_slices * n_rb spread over the SMs (1 CTA/SM at >=114 KB smem).
+void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms) {
+    p.fast = false;
+    if (p.b > 8 || p.m > 4 || !(p.v == 2 || p.v == 4 || p.v == 8 || p.v == 16)) return;
+    p.kbits = p.b <= 4 ? 4 : 8;
+    double best = 1e300;
+    const int us[3] = {4, 2, 1};
+    for (int ui = 0; ui < 3; ++ui) {
+        const int u = us[ui];
+        if (force_u && u != force_u) continue;
+        if (!cg::fused_instantiated(p.v, p.m, u, p.kbits)) continue;
+        const int lg = scale_lg(p, u);
+        if (lg < 0) continue;
+        const int64_t slice_segs = 32LL * u;
+        const int64_t n_slices = (p.segs + slice_segs - 1) / slice_segs;
+        const int64_t n_rg = (p.rows + 15) / 16;
+        const int smem = cg::fused_smem_bytes(p.v, p.m, u, p.kbits);
+        const int occ = std::max(1, std::min(3, (int)(227 * 1024 / (smem + 1024))));
+        int64_t rg_per_task;
+        if (force_rg) {
+            rg_per_task = force_rg;
+        } else {
+            const int64_t want_tasks = (int64_t)sms * occ;
+            int64_t n_rb = std::max<int64_t>(1, (want_tasks + n_slices - 1) / n_slices);
+            rg_per_task = std::max<int64_t>(1, (n_rg + n_rb - 1) / n_rb);
+        }
+        const int64_t n_rb = (n_rg + rg_per_task - 1) / rg_per_task;
+        const int64_t tasks = n_slices * n_rb;
+        const double per_task = (double)rg_per_task * 16.0 * (u * p.m + 1) +
+                                (double)p.m * u * (1 << p.kbits) + 600.0;
+        const double waves = std::ceil((double)tasks / ((double)sms * occ));
+        const double cost = waves * per_task * occ + (n_slices > 1 ? 2000.0 : 0.0);
+        if (cost < best) {
+            best = cost;
+            p.fast = true;
+            p.u = u;
+            p.lg = lg;
+            p.n_gs = 32 >> lg;
+            p.slice_segs = slice_segs;
+            p.n_slices = n_slices;
+            p.rows_pad = n_rg * 16;
+            p.n_rg = n_rg;
+            p.rg_per_task = (int)rg_per_task;
+            p.n_rb = n_rb;
+            p.smem_bytes = smem;
+        }
+    }
+    if (p.fast) {
+        p.code_bytes = p.n_slices * p.n_rg * (int64_t)p.m * 16 * p.slice_segs;
+        p.scale_bytes = p.n_slices * p.n_rg * (int64_t)p.n_gs * 16 * 2;
+    }
+}
+
+}  // namespace
+
+struct cg_layer {
+    cg::Plan plan;
+    int device = 0;
+    uint8_t* codes = nullptr;       // fast layout (plan.fast)
+    uint16_t* raw16 = nullptr;      // (m, rows, segs) when no fast layout
+    uint16_t* scl = nullptr;        // prepacked scale tiles (fast)
+    uint16_t* scales = nullptr;     // (rows, groups) binary16
+    uint16_t* books = nullptr;      // (m, 2**b, v) binary16
+    float* ws = nullptr;            // split-K workspace (n_slices, rows, ws_cols)
+    int ws_cols = 0;
+    uint16_t* x_dev = nullptr;      // staging for the host entry point
+    float* y_dev = nullptr;
+    int stage_cols = 0;
+    uint16_t* x_pin = nullptr;
+    float* y_pin = nullptr;
+    int flags = 0;
+    int64_t device_bytes = 0;
+};
+
+namespace {
+
+template <typename T>
+int dev_alloc(cg_layer* L, T** p, size_t bytes, const char* what) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    L->device_bytes += (int64_t)bytes;
+    return CG_OK;
+}
+
+void free_layer(cg_layer* L) {
+    if (!L) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(L->device);
+    cudaFree(L->codes);
+    cudaFree(L->raw16);
+    cudaFree(L->scl);
+    cudaFree(L->scales);
+    cudaFree(L->books);
+    cudaFree(L->ws);
+    cudaFree(L->x_dev);
+    cudaFree(L->y_dev);
+    cudaFreeHost(L->x_pin);
+    cudaFreeHost(L->y_pin);
+    cudaSetDevice(prev);
+    delete L;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int ensure_ws(cg_layer* L, int n) {
+    const cg::Plan& p = L->plan;
+    if (!p.fast || p.n_slices <= 1 || n <= L->ws_cols) return CG_OK;
+    if (L->ws) {
+        cudaFree(L->ws);
+        L->device_bytes -= (int64_t)p.n_slices * p.rows * L->ws_cols * 4;
+        L->ws = nullptr;
+    }
+    int rc = dev_alloc(L, &L->ws, (size_t)p.n_slices * p.rows * n * 4, "workspace alloc");
+    if (rc) return rc;
+    L->ws_cols = n;
+    return CG_OK;
+}
+
+int run_gemm(cg_layer* L, const uint16_t* x, int n, float* y, int mode, cudaStream_t s) {
+    const cg::Plan& p = L->plan;
+    if (mode == CG_MODE_AUTO) mode = p.fast ? CG_MODE_FAST : CG_MODE_STRICT;
+    if (mode == CG_MODE_FAST && !p.fast)
+        return fail(CG_ERR_UNSUPPORTED,
+                    "no fused kernel for v=%d m=%d b=%d g=%lld at cols=%lld; use CG_MODE_STRICT",
+                    p.v, p.m, p.b, (long long)p.g, (long long)p.cols);
+    if (mode == CG_MODE_STRICT) {
+        CG_CUDA(cg::launch_strict_gemm(p, L->codes, L->raw16, L->books, L->scales, x, n, y, s),
+                "strict kernel launch");
+        return CG_OK;
+    }
+    if (mode != CG_MODE_FAST) return fail(CG_ERR_ARG, "unknown mode %d", mode);
+    int rc = ensure_ws(L, n);
+    if (rc) return rc;
+    const bool split = p.n_slices > 1;
+    const bool pdl = !(L->flags & CG_OPT_NO_PDL);
+    cg::GatherParams gp{};
+    gp.codes = L->codes;
+    gp.scl = L->scl;
+    gp.books = L->books;
+    gp.x = x;
+    gp.out = split ? L->ws : y;
+    gp.rows = p.rows;
+    gp.cols = p.cols;
+    gp.n_rg = p.n_rg;
+    gp.n_slices = p.n_slices;
+    gp.n_rb = p.n_rb;
+    gp.out_slice_stride = split ? p.rows * n : 0;
+    gp.n = n;
+    gp.kcount = p.kcount;
+    gp.rg_per_task = p.rg_per_task;
+    gp.lg = p.lg;
+    gp.n_gs = p.n_gs;
+    gp.flags = (L->flags & CG_OPT_NO_L2_PREFETCH) ? cg::kFlagNoPrefetch : 0;
+    CG_CUDA(cg::launch_fused_gemv(p, gp, pdl, s), "fused gemv launch");
+    if (split)
+        CG_CUDA(cg::launch_reduce_slices(L->ws, y, p.rows * n, p.n_slices, pdl, s),
+                "split-K reduce launch");
+    return CG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cg_abi_version(void) { return CG_ABI_VERSION; }
+
+const char* cg_last_error(void) { return g_last_error.c_str(); }
+
+int cg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
+                    const uint16_t* scales, int64_t rows, int64_t cols, int v, int m, int b,
+                    int64_t g, const cg_layer_options* opts, cg_layer** out) {
+    if (!out) return fail(CG_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (!codes || !books || !scales) return fail(CG_ERR_ARG, "NULL codes/books/scales");
+    // QuantConfig.__post_init__ / validate_shape (quantizer.py:55-84)
+    if (v < 1) return fail(CG_ERR_CONFIG, "v must be >= 1, got %d", v);
+    if (m < 1) return fail(CG_ERR_CONFIG, "m must be >= 1, got %d", m);
+    if (b < 1 || b > 16) return fail(CG_ERR_CONFIG, "b must be in [1, 16], got %d", b);
+    if (g != -1) {
+        if (g < v) return fail(CG_ERR_CONFIG, "g must be >= v (got g=%lld, v=%d)", (long long)g, v);
+        if (g % v) return fail(CG_ERR_CONFIG, "g must be a multiple of v (got g=%lld, v=%d)",
+                               (long long)g, v);
+    }
+    if (rows < 1 || cols < 1)
+        return fail(CG_ERR_CONFIG, "matrix dims must be >= 1, got %lldx%lld", (long long)rows,
+                    (long long)cols);
+    if (cols % v) return fail(CG_ERR_CONFIG, "cols=%lld not divisible by v=%d", (long long)cols, v);
+    const int64_t g_eff = g == -1 ? cols : g;
+    if (cols % g_eff)
+        return fail(CG_ERR_CONFIG, "cols=%lld not divisible by g=%lld", (long long)cols,
+                    (long long)g);
+    for (int t = 0; t < m; ++t)
+        if (!codes[t] || !books[t]) return fail(CG_ERR_ARG, "NULL plane/book %d", t);
+
+    int device = 0;
+    if (opts && opts->device >= 0) device = opts->device;
+    else if (cudaGetDevice(&device) != cudaSuccess) device = 0;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(CG_ERR_CUDA, "no CUDA device available (%s); this library has no CPU path",
+                    cudaGetErrorString(e));
+    if (device >= ndev) return fail(CG_ERR_ARG, "device %d out of range (%d)", device, ndev);
+    DeviceGuard guard(device);
+
+    cg_layer* L = new cg_layer();
+    L->device = device;
+    L->flags = opts ? opts->flags : 0;
+    cg::Plan& p = L->plan;
+    p.rows = rows;
+    p.cols = cols;
+    p.v = v;
+    p.m = m;
+    p.b = b;
+    p.g = g;
+    p.g_row = (g == -1);
+    p.g_eff = g_eff;
+    p.kcount = 1 << b;
+    p.segs = cols / v;
+    p.groups = cols / g_eff;
+    plan_fast(p, opts ? opts->u : 0, opts ? opts->rg_per_task : 0, sm_count_of(device));
+    if (opts && opts->u && !p.fast) {
+        free_layer(L);
+        return fail(CG_ERR_CONFIG, "u=%d is not valid for v=%d m=%d b=%d g=%lld", opts->u, v, m,
+                    b, (long long)g);
+    }
+
+    const size_t plane_elems = (size_t)rows * p.segs;
+    const size_t raw_bytes = plane_elems * m * 2;
+    const size_t scale_elems = (size_t)rows * p.groups;
+    const size_t book_elems = (size_t)p.kcount * v;
+    int rc = CG_OK;
+    uint16_t* raw = nullptr;
+    unsigned* bad = nullptr;
+    cudaStream_t s = nullptr;
+    auto bail = [&](int code) {
+        cudaFree(raw);
+        cudaFree(bad);
+        free_layer(L);
+        return code;
+    };
+    if ((rc = dev_alloc(L, &L->scales, scale_elems * 2, "scales alloc"))) return bail(rc);
+    if ((rc = dev_alloc(L, &L->books, book_elems * m * 2, "books alloc"))) return bail(rc);
+    e = cudaMemcpy(L->scales, scales, scale_elems * 2, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "scales upload"));
+    for (int t = 0; t < m; ++t) {
+        e = cudaMemcpy(L->books + t * book_elems, books[t], book_elems * 2, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "books upload"));
+    }
+    e = cudaMalloc(&raw, raw_bytes ? raw_bytes : 16);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "plane staging alloc"));
+    e = cudaMalloc(&bad, sizeof(unsigned));
+    if (e != cudaSuccess) return bail(cuda_fail(e, "flag alloc"));
+    cudaMemset(bad, 0, sizeof(unsigned));
+    for (int t = 0; t < m; ++t) {
+        e = cudaMemcpy(raw + t * plane_elems, codes[t], plane_elems * 2, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "plane upload"));
+    }
+    if (p.fast) {
+        if ((rc = dev_alloc(L, &L->codes, (size_t)p.code_bytes, "code stream alloc")))
+            return bail(rc);
+        if ((rc = dev_alloc(L, &L->scl, (size_t)p.scale_bytes, "scale tiles alloc")))
+            return bail(rc);
+        e = cg::launch_prepack_codes(p, raw, L->codes, bad, s);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "prepack codes"));
+        e = cg::launch_prepack_scales(p, L->scales, L->scl, s);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "prepack scales"));
+    } else {
+        e = cg::launch_check_codes(p, raw, bad, s);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "check codes"));
+    }
+    unsigned bad_h = 0;
+    e = cudaMemcpy(&bad_h, bad, sizeof bad_h, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "prepack"));
+    if (bad_h) return bail(fail(CG_ERR_INTEGRITY, "code out of range for b=%d", b));
+    if (p.fast) {
+        cudaFree(raw);
+    } else {
+        L->raw16 = raw;  // strict kernel reads the uint16 planes directly
+        L->device_bytes += (int64_t)raw_bytes;
+    }
+    raw = nullptr;
+    cudaFree(bad);
+    bad = nullptr;
+    if (p.fast && p.n_slices > 1) {
+        if ((rc = ensure_ws(L, 1))) return bail(rc);
+    }
+    *out = L;
+    return CG_OK;
+}
+
+int cg_layer_destroy(cg_layer* layer) {
+    free_layer(layer);
+    return CG_OK;
+}
+
+int cg_layer_query(const cg_layer* L, cg_layer_info* info) {
+    if (!L || !info) return fail(CG_ERR_ARG, "NULL layer/info");
+    const cg::Plan& p = L->plan;
+    std::memset(info, 0, sizeof *info);
+    info->rows = p.rows;
+    info->cols = p.cols;
+    info->v = p.v;
+    info->m = p.m;
+    info->b = p.b;
+    info->g = p.g;
+    info->fast_supported = p.fast ? 1 : 0;
+    info->u = p.u;
+    info->rg_per_task = p.rg_per_task;
+    info->n_slices = p.n_slices;
+    info->n_tasks = p.fast ? p.n_slices * p.n_rb : 0;
+    info->smem_bytes = p.smem_bytes;
+    info->launches_fast = p.fast ? (p.n_slices > 1 ? 2 : 1) : 0;
+    info->device_bytes = L->device_bytes;
+    // codes at b bits + binary16 scales + binary16 codebooks
+    info->algorithmic_bytes = (p.rows * p.segs * p.m * p.b + 7) / 8 + 2 * p.rows * p.groups +
+                              2LL * p.m * p.kcount * p.v;
+    return CG_OK;
+}
+
+int cg_layer_gemm(cg_layer* L, const void* x, int n, float* y, int mode, void* stream) {
+    if (!L || !x || !y) return fail(CG_ERR_ARG, "NULL layer/x/y");
+    if (n < 1) return fail(CG_ERR_SHAPE, "x must have >= 1 column, got %d", n);
+    DeviceGuard guard(L->device);
+    return run_gemm(L, static_cast<const uint16_t*>(x), n, y, mode,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int cg_layer_gemm_host(cg_layer* L, const uint16_t* x, int n, float* y, int mode, void* stream) {
+    if (!L || !x || !y) return fail(CG_ERR_ARG, "NULL layer/x/y");
+    if (n < 1) return fail(CG_ERR_SHAPE, "x must have >= 1 column, got %d", n);
+    DeviceGuard guard(L->device);
+    const cg::Plan& p = L->plan;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t xb = (size_t)p.cols * n * 2, yb = (size_t)p.rows * n * 4;
+    if (n > L->stage_cols) {
+        cudaFree(L->x_dev);
+        cudaFree(L->y_dev);
+        cudaFreeHost(L->x_pin);
+        cudaFreeHost(L->y_pin);
+        L->x_dev = nullptr;
+        L->y_dev = nullptr;
+        L->x_pin = nullptr;
+        L->y_pin = nullptr;
+        CG_CUDA(cudaMalloc(&L->x_dev, xb), "x staging alloc");
+        CG_CUDA(cudaMalloc(&L->y_dev, yb), "y staging alloc");
+        CG_CUDA(cudaHostAlloc(&L->x_pin, xb, cudaHostAllocDefault), "pinned x alloc");
+        CG_CUDA(cudaHostAlloc(&L->y_pin, yb, cudaHostAllocDefault), "pinned y alloc");
+        L->stage_cols = n;
+    }
+    std::memcpy(L->x_pin, x, xb);
+    CG_CUDA(cudaMemcpyAsync(L->x_dev, L->x_pin, xb, cudaMemcpyHostToDevice, s), "x H2D");
+    int rc = run_gemm(L, L->x_dev, n, L->y_dev, mode, s);
+    if (rc) return rc;
+    CG_CUDA(cudaMemcpyAsync(L->y_pin, L->y_dev, yb, cudaMemcpyDeviceToHost, s), "y D2H");
+    CG_CUDA(cudaStreamSynchronize(s), "gemm");
+    std::memcpy(y, L->y_pin, yb);
+    return CG_OK;
+}
+
+int cg_layer_psumbook(cg_layer* L, const void* x, int n, float* out, void* stream) {
+    if (!L || !x || !out) return fail(CG_ERR_ARG, "NULL layer/x/out");
+    if (n < 1) return fail(CG_ERR_SHAPE, "x must have >= 1 column, got %d", n);
+    const cg::Plan& p = L->plan;
+    if (!p.fast) return fail(CG_ERR_UNSUPPORTED, "layer has no fused kernel");
+    DeviceGuard guard(L->device);
+    cg::GatherParams gp{};
+    gp.books = L->books;
+    gp.x = static_cast<const uint16_t*>(x);
+    gp.cols = p.cols;
+    gp.n = n;
+    gp.kcount = p.kcount;
+    CG_CUDA(cg::launch_psumbook_dump(p, gp, out, static_cast<cudaStream_t>(stream)),
+            "psumbook dump launch");
+    return CG_OK;
+}
+
+int cg_layer_unpack_codes(cg_layer* L, uint16_t* out, void* stream) {
+    if (!L || !out) return fail(CG_ERR_ARG, "NULL layer/out");
+    DeviceGuard guard(L->device);
+    CG_CUDA(cg::launch_unpack_codes(L->plan, L->codes, L->raw16, out,
+                                    static_cast<cudaStream_t>(stream)),
+            "unpack launch");
+    return CG_OK;
+}
+
+int cg_psumbook_build(const void* books, const void* x, int m, int b, int v, int64_t k_len, int n,
+                      float* out, void* stream) {
+    if (!books || !x || !out) return fail(CG_ERR_ARG, "NULL books/x/out");
+    if (m < 1 || v < 1 || b < 1 || b > 16) return fail(CG_ERR_CONFIG, "bad m/v/b");
+    if (k_len < 1 || k_len % v)
+        return fail(CG_ERR_CONFIG, "tile width %lld not divisible by v=%d", (long long)k_len, v);
+    if (n < 1) return fail(CG_ERR_SHAPE, "n must be >= 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(CG_ERR_CUDA, "no CUDA device available; this library has no CPU path");
+    CG_CUDA(cg::launch_psumbook_build(static_cast<const uint16_t*>(books),
+                                      static_cast<const uint16_t*>(x), m, b, v, k_len, n, out,
+                                      static_cast<cudaStream_t>(stream)),
+            "psumbook build launch");
+    return CG_OK;
+}
+
+}  // extern "C"

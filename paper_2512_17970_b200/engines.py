@@ -1,0 +1,306 @@
+"""Drop-in replacement of the reference's CodeGEMM engine API, on B200.
+
+Reference interface (``/root/reference/pkg/src/codegemm/engines.py``):
+
+* ``TileConfig``       engines.py:46-69   -- same fields and validation rules
+* ``OpCounters``       engines.py:72-84   -- same event tallies (closed forms)
+* ``phase_split``      engines.py:87-97
+* ``Psumbook``         engines.py:100-112
+* ``build_psumbook``   engines.py:137-156 -- runs the sm_100a Psumbook kernel
+* ``codegemm_gemm``    engines.py:245-316 -- runs the fused sm_100a GEMV
+
+``codegemm_gemm(q, x, tiles=None, threads=1)`` keeps the reference signature,
+argument checks and error classes, and returns ``(float32 (rows, N),
+OpCounters)``.  The layer's planes are uploaded and prepacked once per layer
+object (weights are static) and cached; every call copies x in and y out.
+
+Numerics: ``mode="fast"`` (default ``"auto"`` picks it when a fused kernel
+exists for the config) builds the Psumbook bit-exactly and accumulates in
+binary32 in a different order than the reference -- parity within the
+tolerance in DESIGN.md §5.  ``mode="strict"`` reproduces the reference's
+binary32 operation order exactly (bit-identical output).  ``tiles`` and
+``threads`` are validated and fold into the counters exactly as in the
+reference, but do not steer the GPU kernel (the reference's own output bits
+are independent of both, engines.py:15-22).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import weakref
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, ShapeError
+
+DEFAULT_TILE_WIDTH = 32
+DEFAULT_TILE_HEIGHT = 2048
+
+
+@dataclass(frozen=True)
+class TileConfig:
+    """t_w elements along K per tile, t_h rows per row block."""
+
+    t_w: int = DEFAULT_TILE_WIDTH
+    t_h: int = DEFAULT_TILE_HEIGHT
+
+    def __post_init__(self):
+        if self.t_w < 1 or self.t_h < 1:
+            raise ConfigError(f"tile dims must be >= 1, got ({self.t_w}, {self.t_h})")
+
+    def validate_for(self, cfg) -> None:
+        v, g = cfg.v, cfg.g
+        if self.t_w < v or self.t_w % v:
+            raise ConfigError(f"t_w={self.t_w} must be a multiple of v={v} and >= v")
+        if g == -1:
+            return
+        inside = self.t_w <= g and g % self.t_w == 0
+        if not (inside or self.t_w % g == 0):
+            raise ConfigError(f"t_w={self.t_w} straddles group boundaries for g={g}")
+
+
+@dataclass
+class OpCounters:
+    mac_build: int = 0
+    mac_read_adds: int = 0
+    lookups: int = 0
+    mac_dense: int = 0
+    psum_entries_per_tile: int = 0
+
+    @property
+    def build_fraction(self) -> float:
+        return phase_split(self)[0]
+
+
+def phase_split(counters) -> tuple[float, float]:
+    """(build, read) shares of table-phase MACs; ValueError if both are 0."""
+    total = counters.mac_build + counters.mac_read_adds
+    if total == 0:
+        raise ValueError("no build/read operations recorded")
+    share = Fraction(counters.mac_build, total)
+    return float(share), float(1 - share)
+
+
+@dataclass
+class Psumbook:
+    """entries[t, j, i]: binary32 dot of centroid i of book t with segment j."""
+
+    entries: np.ndarray  # (m, t_w // v, 2**b) float32
+
+    @property
+    def entry_count(self) -> int:
+        return int(self.entries.size)
+
+
+def closed_form_counters(rows: int, cols: int, n: int, v: int, m: int, b: int,
+                         t_w: int) -> OpCounters:
+    """The tallies codegemm_gemm reports (engines.py:300-316, accounting.py:109-126)."""
+    events = m * rows * (cols // v) * n
+    return OpCounters(
+        mac_build=m * (1 << b) * cols * n,
+        mac_read_adds=events,
+        lookups=events,
+        psum_entries_per_tile=m * (1 << b) * (min(t_w, cols) // v),
+    )
+
+
+# ---------------------------------------------------------------------------
+# device-resident layer (one handle of the C library)
+# ---------------------------------------------------------------------------
+
+def _layer_arrays(q):
+    """(codes, books, scales) host arrays of a QuantizedLayer-like object."""
+    codes = [np.ascontiguousarray(p.codes, dtype=np.uint16) for p in q.planes]
+    books = [np.ascontiguousarray(np.asarray(bk.entries).view(np.uint16)) for bk in q.books]
+    scales = np.ascontiguousarray(np.asarray(q.scales.scales).view(np.uint16))
+    return codes, books, scales
+
+
+class DeviceLayer:
+    """A quantized layer uploaded, prepacked and resident on one B200.
+
+    ``row_range=(r0, r1)`` uploads only those output rows (a row shard; see
+    ``dist.py``).  ``u`` / ``rg_per_task`` override the planner's tiling.
+    """
+
+    def __init__(self, q, *, row_range=None, u: int = 0, rg_per_task: int = 0,
+                 flags: int = 0, device: int = -1):
+        lib = _lib.load()
+        cfg = q.config
+        codes, books, scales = _layer_arrays(q)
+        r0, r1 = (0, q.rows) if row_range is None else (int(row_range[0]), int(row_range[1]))
+        if not 0 <= r0 < r1 <= q.rows:
+            raise ShapeError(f"row range {(r0, r1)} outside 0..{q.rows}")
+        codes = [np.ascontiguousarray(c[r0:r1]) for c in codes]
+        scales = np.ascontiguousarray(scales[r0:r1])
+        self.rows, self.cols = r1 - r0, int(q.cols)
+        self.row_range = (r0, r1)
+        self.v, self.m, self.b, self.g = int(cfg.v), int(cfg.m), int(cfg.b), int(cfg.g)
+        self._keep = (codes, books, scales)
+        code_ptrs = (ctypes.c_void_p * self.m)(*[c.ctypes.data for c in codes])
+        book_ptrs = (ctypes.c_void_p * self.m)(*[bk.ctypes.data for bk in books])
+        opts = _lib.LayerOptions(u=u, rg_per_task=rg_per_task, flags=flags, device=device)
+        handle = ctypes.c_void_p()
+        _lib.check(lib.cg_layer_create(code_ptrs, book_ptrs, scales.ctypes.data,
+                                       self.rows, self.cols, self.v, self.m, self.b,
+                                       self.g, ctypes.byref(opts), ctypes.byref(handle)))
+        self._keep = None  # the library copied what it needs
+        self._handle = handle
+        self._lib = lib
+        info = _lib.LayerInfo()
+        _lib.check(lib.cg_layer_query(handle, ctypes.byref(info)))
+        self.info = info.as_dict()
+
+    # -- lifetime -----------------------------------------------------------
+    def close(self) -> None:
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value:
+            self._lib.cg_layer_destroy(h)
+        self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._handle
+
+    # -- host buffers -------------------------------------------------------
+    def gemm_host(self, x_f16: np.ndarray, mode: str = "auto") -> np.ndarray:
+        x = np.ascontiguousarray(x_f16, dtype=np.float16)
+        if x.ndim != 2 or x.shape[0] != self.cols:
+            raise ShapeError(f"layer is {self.rows}x{self.cols} but X is {x.shape}")
+        n = int(x.shape[1])
+        y = np.empty((self.rows, n), dtype=np.float32)
+        _lib.check(self._lib.cg_layer_gemm_host(self._handle, x.ctypes.data, n, y.ctypes.data,
+                                                _lib.MODES[mode], None))
+        return y
+
+    # -- device buffers (torch) --------------------------------------------
+    def gemm(self, x, y=None, mode: str = "auto", stream=None):
+        """y (rows, n) float32 = W @ x for a CUDA float16 tensor x (cols, n)."""
+        import torch
+
+        if x.dtype != torch.float16 or not x.is_cuda or x.dim() != 2 or x.shape[0] != self.cols:
+            raise ShapeError(f"x must be a CUDA float16 ({self.cols}, n) tensor, got "
+                             f"{tuple(x.shape)} {x.dtype}")
+        x = x.contiguous()
+        n = int(x.shape[1])
+        if y is None:
+            y = torch.empty((self.rows, n), dtype=torch.float32, device=x.device)
+        s = stream if stream is not None else torch.cuda.current_stream(x.device)
+        _lib.check(self._lib.cg_layer_gemm(self._handle, x.data_ptr(), n, y.data_ptr(),
+                                           _lib.MODES[mode], ctypes.c_void_p(s.cuda_stream)))
+        return y
+
+    def psumbook(self, x, stream=None):
+        """The fused kernel's shared-memory Psumbook, (m, cols/v, 2**b, n) float32."""
+        import torch
+
+        x = x.contiguous()
+        n = int(x.shape[1])
+        out = torch.empty((self.m, self.cols // self.v, 1 << self.b, n), dtype=torch.float32,
+                          device=x.device)
+        s = stream if stream is not None else torch.cuda.current_stream(x.device)
+        _lib.check(self._lib.cg_layer_psumbook(self._handle, x.data_ptr(), n, out.data_ptr(),
+                                               ctypes.c_void_p(s.cuda_stream)))
+        return out
+
+    def unpack_codes(self, stream=None) -> np.ndarray:
+        """Per-row gather indices read back from the prepacked device stream."""
+        import torch
+
+        out = torch.empty((self.m, self.rows, self.cols // self.v), dtype=torch.int16,
+                          device=f"cuda:{torch.cuda.current_device()}")
+        s = stream if stream is not None else torch.cuda.current_stream()
+        _lib.check(self._lib.cg_layer_unpack_codes(self._handle, out.data_ptr(),
+                                                   ctypes.c_void_p(s.cuda_stream)))
+        return out.cpu().numpy().view(np.uint16)
+
+
+# one device copy per live layer object (weights are immutable)
+_CACHE: dict = {}
+
+
+def device_layer_for(q) -> DeviceLayer:
+    key = id(q)
+    hit = _CACHE.get(key)
+    if hit is not None and hit[0]() is q:
+        return hit[1]
+    dl = DeviceLayer(q)
+    try:
+        ref = weakref.ref(q, lambda _r, k=key: _CACHE.pop(k, None))
+    except TypeError:  # not weak-referenceable: keep the layer alive instead
+        ref = (lambda obj: (lambda: obj))(q)
+    _CACHE[key] = (ref, dl)
+    return dl
+
+
+# ---------------------------------------------------------------------------
+# the reference-facing operator API
+# ---------------------------------------------------------------------------
+
+def _x_array(x) -> np.ndarray:
+    data = getattr(x, "data", x)
+    return np.asarray(data)
+
+
+def codegemm_gemm(q, x, tiles: TileConfig | None = None, threads: int = 1, *,
+                  mode: str = "auto"):
+    """Y = W @ X through the sm_100a kernels; reference signature and errors.
+
+    Checks in the reference's order (engines.py:264-269): shape, tiling,
+    thread count.  Returns (float32 (q.rows, x.cols), OpCounters).
+    """
+    xa = _x_array(x)
+    if xa.ndim != 2 or q.cols != xa.shape[0]:
+        raise ShapeError(f"layer is {q.rows}x{q.cols} but X is "
+                         f"{xa.shape[0] if xa.ndim == 2 else '?'}x"
+                         f"{xa.shape[1] if xa.ndim == 2 else '?'}")
+    tiles = tiles if tiles is not None else TileConfig()
+    cfg = q.config
+    tiles.validate_for(cfg)
+    if threads < 1:
+        raise ConfigError(f"threads must be >= 1, got {threads}")
+    if mode not in _lib.MODES:
+        raise ConfigError(f"unknown mode {mode!r}")
+    y = device_layer_for(q).gemm_host(xa, mode)
+    counters = closed_form_counters(q.rows, q.cols, int(xa.shape[1]), cfg.v, cfg.m, cfg.b,
+                                    tiles.t_w)
+    return y, counters
+
+
+def build_psumbook(x_tile, books, counters=None) -> Psumbook:
+    """Psumbook of one input column on the GPU (engines.py:137-156), bit-exact."""
+    import torch
+
+    books = list(books)
+    if not books:
+        raise ConfigError("at least one codebook required")
+    ents = [np.asarray(getattr(bk, "entries", bk)) for bk in books]
+    v = int(ents[0].shape[1])
+    x16 = np.asarray(x_tile, dtype=np.float16).reshape(-1)
+    if x16.size == 0 or x16.size % v:
+        raise ConfigError(f"tile width {x16.size} not divisible by v={v}")
+    k = int(ents[0].shape[0])
+    b = k.bit_length() - 1
+    lib = _lib.load()
+    dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+    if dev is None:
+        _lib.check(lib.cg_psumbook_build(None, None, 1, 1, 1, 1, 1, None, None))
+    bk_t = torch.from_numpy(np.concatenate([e.astype(np.float16).reshape(-1) for e in ents])).to(dev)
+    x_t = torch.from_numpy(x16.copy()).to(dev)
+    out = torch.empty((len(ents), x16.size // v, k, 1), dtype=torch.float32, device=dev)
+    s = torch.cuda.current_stream(dev)
+    _lib.check(lib.cg_psumbook_build(bk_t.data_ptr(), x_t.data_ptr(), len(ents), b, v,
+                                     x16.size, 1, out.data_ptr(), ctypes.c_void_p(s.cuda_stream)))
+    entries = out[..., 0].cpu().numpy()
+    if counters is not None:
+        counters.mac_build += len(ents) * k * x16.size
+    return Psumbook(entries)
