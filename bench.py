@@ -1,0 +1,462 @@
+"""Benchmark of the B200 CodeGEMM decode GEMV (driver contract: one JSON line).
+
+Metric (BASELINE.json): "us/layer & HBM GB/s (frac of roofline), 2-bit
+Llama-3 8B/70B decode, batch 1".  ``value`` is whole-job HBM throughput in
+GB/s: algorithmic bytes (codes at b bits + binary16 scales + binary16
+codebooks + x + y) of every layer in one decoder block, divided
+by the device time of the block.  Per-layer microseconds are in ``us_per_layer``.
+
+Workloads (a "step" = the linear layers of one decoder block, the
+reference's bench suite with its multiplicities, bench.py:63-74):
+  8b  (default at N=1) : 4 x 4096x4096, 2 x 14336x4096, 1 x 4096x14336
+  70b (default at N>1) : 4 x 8192x8192, 2 x 28672x8192, 1 x 8192x28672, rows
+                         sharded over the N GPUs + NCCL all-gather per layer
+Every layer of a step has its own weights; steps rotate through enough
+distinct copies of the block that the weight stream is larger than L2
+(inputs larger than L2: no cache flush needed).  Steps are replayed from CUDA
+graphs; time is CUDA events on the launching stream, max over ranks.
+
+``--impl reference`` times the reference's CPU algorithm (the oracle port of
+engines.py:245-316, oracle/codegemm_oracle.py) on a bounded sample of the same
+workload on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "μs/layer & HBM GB/s (frac of roofline), 2-bit Llama-3 8B/70B decode, batch 1"
+L2_BYTES = 126 * 1024 * 1024
+CONFIGS = {"m1v4g128": dict(v=4, m=1, b=8, g=128), "m2v8g128": dict(v=8, m=2, b=8, g=128)}
+SUITES = {
+    "8b": (("attn_proj", 4096, 4096, 4), ("mlp_gate_up", 14336, 4096, 2),
+           ("mlp_down", 4096, 14336, 1)),
+    "70b": (("attn_proj", 8192, 8192, 4), ("mlp_gate_up", 28672, 8192, 2),
+            ("mlp_down", 8192, 28672, 1)),
+}
+
+
+def layer_bytes(rows: int, cols: int, cfg: dict, n: int, with_io: bool = True) -> int:
+    """Algorithmic HBM bytes of one layer call."""
+    v, m, b, g = cfg["v"], cfg["m"], cfg["b"], cfg["g"]
+    codes = (rows * (cols // v) * m * b + 7) // 8
+    scales = 2 * rows * (cols // (cols if g == -1 else g))
+    books = 2 * m * (1 << b) * v
+    io = 2 * cols * n + 4 * rows * n if with_io else 0
+    return codes + scales + books + io
+
+
+def block_spec(workload: str):
+    return [(name, rows, cols) for (name, rows, cols, mult) in SUITES[workload] for _ in range(mult)]
+
+
+def make_layer(rows, cols, cfg, seed):
+    import paper_2512_17970_b200 as cg
+
+    qc = cg.QuantConfig(v=cfg["v"], m=cfg["m"], b=cfg["b"], g=cfg["g"])
+    return cg.random_layer(rows, cols, qc, seed=seed)
+
+
+def layer_seed(copy: int, idx: int, rows: int, cols: int) -> int:
+    # copy 0, first layer of each shape: the reference's bench_layer seed (bench.py:168-170)
+    return (0 ^ rows ^ cols) if copy == 0 and idx == 0 else 1_000_003 * (copy + 1) + 7919 * idx
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled while the timed region runs."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "50", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not self.path or not os.path.exists(self.path):
+            return None
+        rows = []
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+
+        def num(s):
+            try:
+                return float(s)
+            except ValueError:
+                return None
+
+        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
+        mx = [num(r[2]) for r in rows if num(r[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- CPU
+def cpu_baseline(spec, cfg, n, budget_s: float = 20.0):
+    """The oracle port (reference algorithm, oracle/codegemm_oracle.py) on host cores."""
+    from oracle import c_oracle
+    from oracle import codegemm_oracle as orc
+
+    # numpy port: the reference's own vectorisation (engines.py:245-316), 1 thread
+    # (its ThreadPool is GIL-bound: threads>1 is slower)
+    done_bytes, t_used, layers_done = 0, 0.0, 0
+    for idx, (name, rows, cols) in enumerate(spec):
+        q = make_layer(rows, cols, cfg, layer_seed(0, idx, rows, cols))
+        x = orc.bench_input_array(cols, n, 0)
+        codes = [p.codes for p in q.planes]
+        books = [b.entries for b in q.books]
+        t0 = time.perf_counter()
+        orc.codegemm(codes, books, q.scales.scales, x, cfg["v"], cfg["g"], 32, 2048)
+        t_used += time.perf_counter() - t0
+        done_bytes += layer_bytes(rows, cols, cfg, n)
+        layers_done += 1
+        if t_used > budget_s:
+            break
+    port = {"value": round(done_bytes / t_used / 1e9, 4), "unit": "GB/s", "cores": 1,
+            "kind": "port",
+            "sample": f"{layers_done} layers of one decoder block through the numpy restatement "
+                      f"of codegemm_gemm, threads=1 ({t_used:.1f} s)"}
+    # C restatement, all host threads (a stronger CPU reference point, same bits)
+    threads = os.cpu_count() or 1
+    done_bytes, t_used = 0, 0.0
+    for idx, (name, rows, cols) in enumerate(spec):
+        q = make_layer(rows, cols, cfg, layer_seed(0, idx, rows, cols))
+        x = orc.bench_input_array(cols, n, 0)
+        t0 = time.perf_counter()
+        c_oracle.codegemm([p.codes for p in q.planes], [b.entries for b in q.books],
+                          q.scales.scales, x, cfg["v"], cfg["g"], 32, threads)
+        t_used += time.perf_counter() - t0
+        done_bytes += layer_bytes(rows, cols, cfg, n)
+    port_c = {"value": round(done_bytes / t_used / 1e9, 4), "unit": "GB/s", "cores": threads,
+              "kind": "port", "sample": "one decoder block through the C restatement "
+                                         f"(oracle/cg_oracle.c), {threads} pthreads"}
+    return port, port_c
+
+
+def run_reference(args, spec, cfg, n, rank, world):
+    """--impl reference: the reference CPU algorithm (oracle port), rank 0 only."""
+    if rank != 0:
+        return
+    from oracle import codegemm_oracle as orc
+
+    # bounded sample: whole layers for 8B, a row sample of each layer for 70B
+    frac = 1 if args.workload == "8b" else 8
+    jobs = []
+    for idx, (name, rows, cols) in enumerate(spec):
+        q = make_layer(rows, cols, cfg, layer_seed(0, idx, rows, cols))
+        r = rows // frac
+        codes = [np.ascontiguousarray(p.codes[:r]) for p in q.planes]
+        jobs.append((codes, [b.entries for b in q.books], np.ascontiguousarray(q.scales.scales[:r]),
+                     orc.bench_input_array(cols, n, 0), r, cols))
+    step_bytes = sum(layer_bytes(r, c, cfg, n) for (_, _, _, _, r, c) in jobs)
+
+    def step():
+        for codes, books, scales, x, r, c in jobs:
+            orc.codegemm(codes, books, scales, x, cfg["v"], cfg["g"], 32, 2048)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = step_bytes * args.steps / dt / 1e9
+    sample = (f"per step: the {len(jobs)} layers of one {args.workload} decoder block"
+              + ("" if frac == 1 else f", first 1/{frac} of each layer's rows")
+              + " through the numpy restatement of codegemm_gemm (engines.py:245-316), threads=1 "
+                "(the reference's ThreadPool is GIL-bound; 1 thread is its fastest setting)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u8/f16->f32",
+        "data": "synthetic (reference generators: random_layer, bench_input)",
+        "config": {"workload": f"llama{args.workload} decoder-block linears, {args.config}, "
+                               f"batch {n}", "config": args.config, "batch": n},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--workload", choices=("auto", "8b", "70b"), default="auto")
+    ap.add_argument("--config", choices=tuple(CONFIGS), default="m1v4g128")
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--detail", action="store_true", help="also time every unique shape alone")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload == "auto":
+        args.workload = "8b" if world == 1 else "70b"
+    cfg = CONFIGS[args.config]
+    n = args.batch
+    spec = block_spec(args.workload)
+    if args.warmup < 3:
+        args.warmup = 3
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.impl == "reference":
+        run_reference(args, spec, cfg, n, rank, world)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import paper_2512_17970_b200 as cg
+    from paper_2512_17970_b200.dist import ShardedLayer
+    from oracle import codegemm_oracle as orc
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    step_bytes = sum(layer_bytes(r, c, cfg, n) for (_, r, c) in spec)
+    weight_bytes = sum(layer_bytes(r, c, cfg, n, with_io=False) for (_, r, c) in spec) // world
+    copies = max(2, -(-3 * L2_BYTES // max(1, weight_bytes)))
+
+    # ---- layers: `copies` distinct copies of the block, rows sharded over ranks
+    blocks = []
+    for cp in range(copies):
+        layers = []
+        for idx, (name, rows, cols) in enumerate(spec):
+            q = make_layer(rows, cols, cfg, layer_seed(cp, idx, rows, cols))
+            sl = ShardedLayer(q, rank, world) if world > 1 else cg.DeviceLayer(q)
+            x = torch.from_numpy(orc.bench_input_array(cols, n, cp * 31 + idx)).to(dev)
+            per = sl.per if world > 1 else rows
+            layers.append({"name": name, "rows": rows, "cols": cols, "layer": sl, "x": x,
+                           "y_local": torch.empty((per, n), dtype=torch.float32, device=dev),
+                           "y": torch.empty((per * world, n), dtype=torch.float32, device=dev)})
+        blocks.append(layers)
+
+    def dev_layer(L):
+        return L["layer"].device_layer if world > 1 else L["layer"]
+
+    def run_kernel(L):
+        dl = dev_layer(L)
+        if dl is not None:
+            dl.gemm(L["x"], L["y_local"] if world > 1 else L["y"])
+
+    def run_layer(L):
+        run_kernel(L)
+        if world > 1:
+            dist.all_gather_into_tensor(L["y"], L["y_local"])
+
+    stream = torch.cuda.Stream(dev)
+
+    def capture(fn):
+        # warm the path (kernel attributes, NCCL communicators) outside capture
+        with torch.cuda.stream(stream):
+            fn()
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        return g
+
+    graphs = [capture(lambda b=b: [run_layer(L) for L in b]) for b in blocks]
+    launches_per_step = sum(dev_layer(L).info["launches_fast"] if dev_layer(L) else 0
+                            for L in blocks[0])
+
+    def timed(replays, count):
+        """Replay graphs[i % len] `count` times; device ms (max over ranks)."""
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for i in range(count):
+                replays[i % len(replays)].replay()
+            ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms
+
+    # ---- warmup + timed region (clocks sampled during it)
+    timed(graphs, args.warmup)
+    soak = 0
+    with ClockSampler(local_rank) as clk:
+        ms = timed(graphs, args.steps)
+        if ms < 1000.0:  # too short for 50 ms sampling: keep the same load running ~1 s
+            soak = int(args.steps * (1000.0 - ms) / max(ms, 1e-3)) + 1
+            timed(graphs, soak)
+    clocks = clk.summary()
+    if clocks is not None and soak:
+        clocks["note"] = (f"timed region {ms:.1f} ms; sampling continued over {soak} more "
+                          "identical steps right after it")
+    ms_per_step = ms / args.steps
+    value = step_bytes * args.steps / (ms / 1e3) / 1e9
+
+    # ---- per-shape microseconds + the dominant kernel alone (one fused launch per layer)
+    uniq = []
+    for idx, (name, rows, cols) in enumerate(spec):
+        if name not in [u[0] for u in uniq]:
+            uniq.append((name, idx, rows, cols))
+    reps = max(20, min(400, args.steps // 4))
+    us_per_layer, kern = {}, {}
+    for name, idx, rows, cols in uniq:
+        gl = [capture(lambda L=b[idx]: run_layer(L)) for b in blocks]
+        us_per_layer[f"{name} {rows}x{cols}"] = round(timed(gl, reps) / reps * 1e3, 3)
+        if dev_layer(blocks[0][idx]) is not None:
+            gk = [capture(lambda L=b[idx]: run_kernel(L)) for b in blocks]
+            kern[name] = (timed(gk, reps) / reps * 1e3, rows, cols, idx)
+        del gl
+    # dominant kernel: the largest per-launch byte count (mlp_gate_up)
+    dom = max(kern, key=lambda k: layer_bytes(kern[k][1] // world, kern[k][2], cfg, n))
+    dom_us, dom_rows, dom_cols, dom_idx = kern[dom]
+    dom_bytes = layer_bytes(-(-dom_rows // world), dom_cols, cfg, n)
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured"
+    else:
+        peak, peak_src = 6650.0, "fallback"
+    achieved = dom_bytes / (dom_us * 1e-6) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{args.config}:{dom_rows}x{dom_cols}")
+        except Exception:
+            traffic = None
+    dl_dom = dev_layer(blocks[0][dom_idx])
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                "kernel": f"fused_gemv_kernel {dom} {dom_rows // world}x{dom_cols} "
+                          f"(u={dl_dom.info['u']}, tasks={dl_dom.info['n_tasks']})",
+                "us_per_launch": round(dom_us, 3), "bytes_per_launch": dom_bytes,
+                "frac_of_8TBs_nominal": round(achieved / 8000.0, 4)}
+
+    # ---- end to end through the reference-facing C ABI with host buffers
+    e2e_steps = max(3, min(args.steps, 100))
+    host_x = [orc.bench_input_array(c, n, 100 + i) for i, (_, r, c) in enumerate(spec)]
+    h2d = sum(x.nbytes for x in host_x)
+    d2h = sum(4 * r * n for (_, r, c) in spec)
+
+    def e2e_step(b):
+        for L, xh in zip(b, host_x):
+            if world > 1:
+                xt = torch.from_numpy(xh).to(dev, non_blocking=False)
+                y = L["layer"].forward(xt)
+                y.cpu()
+            else:
+                L["layer"].gemm_host(xh)
+
+    e2e_step(blocks[0])
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        e2e_step(blocks[i % len(blocks)])
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": round(step_bytes * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "ms_per_step": round(e2e_s / e2e_steps * 1e3, 3),
+           "path": "cg_layer_gemm_host per layer (pinned staging, H2D x, kernels, D2H y, sync)"
+           if world == 1 else "ShardedLayer.forward per layer (H2D x, kernels, NCCL all-gather, D2H y)"}
+
+    base = base_c = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base, base_c = cpu_baseline(spec, cfg, n)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "u8 codes, f16 in, f32 accumulate",
+            "data": "synthetic (reference generators random_layer/bench_input; random codebooks, "
+                    "codes, scales)",
+            "config": {"workload": f"llama{args.workload} decoder-block linears (reference suite "
+                                   f"x multiplicity), {args.config}, batch {n}",
+                       "config": args.config, "batch": n,
+                       "layers_per_step": len(spec), "weight_copies": copies,
+                       "l2": f"inputs larger than L2: {copies} distinct block copies rotated "
+                             f"({copies * weight_bytes / 2**20:.0f} MiB of weights per rank)",
+                       "parallelism": f"rows sharded over {world} GPUs + NCCL all-gather"
+                       if world > 1 else "single GPU", "graphs": "CUDA graph per block copy, PDL"},
+            "us_per_layer": us_per_layer,
+            "us_per_block": round(ms_per_step * 1e3, 3),
+            "roofline": roofline,
+            "cpu_baseline": base, "cpu_baseline_c": base_c,
+            "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -75,7 +76,7 @@ int scale_lg(const cg::Plan& p, int u) {
 //   gather  = rows/16 * 16*(u*m + 1)   (one LDS per lookup + SHFL reduction)
 //   build   = m*u*2**kb                (STS.128 of the slice tables)
 // with tasks = n_slices * n_rb spread over the SMs (1 CTA/SM at >=114 KB smem).
-void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms) {
+void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms, int reserved) {
     p.fast = false;
     if (p.b > 8 || p.m > 4 || !(p.v == 2 || p.v == 4 || p.v == 8 || p.v == 16)) return;
     p.kbits = p.b <= 4 ? 4 : 8;
@@ -90,22 +91,44 @@ void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms) {
         const int64_t slice_segs = 32LL * u;
         const int64_t n_slices = (p.segs + slice_segs - 1) / slice_segs;
         const int64_t n_rg = (p.rows + 15) / 16;
-        const int smem = cg::fused_smem_bytes(p.v, p.m, u, p.kbits);
-        const int occ = std::max(1, std::min(3, (int)(227 * 1024 / (smem + 1024))));
+        cg::FusedSizes z;
+        if (!cg::fused_sizes(p.v, p.m, u, p.kbits, &z)) continue;
+        const int n_gs = 32 >> lg;
+        // rows per task are capped by the smem left for the task's scale tiles
+        int64_t rg_cap = 0;
+        {
+            cg::SmemLayout lay;
+            int64_t lo = 0, hi = 1 << 16;
+            while (lo < hi) {  // largest rg count whose layout fits
+                const int64_t mid = (lo + hi + 1) / 2;
+                if (cg::smem_layout(z, (int)(mid * n_gs * 32), reserved, &lay)) lo = mid;
+                else hi = mid - 1;
+            }
+            rg_cap = lo;
+        }
+        if (rg_cap < 1) continue;
+        const int occ = 1;  // 512 threads x >100 registers: one CTA per SM
         int64_t rg_per_task;
         if (force_rg) {
             rg_per_task = force_rg;
         } else {
+            // fill exactly one wave: tasks = n_slices * n_rb <= sms * occ
             const int64_t want_tasks = (int64_t)sms * occ;
-            int64_t n_rb = std::max<int64_t>(1, (want_tasks + n_slices - 1) / n_slices);
+            int64_t n_rb = std::max<int64_t>(1, want_tasks / n_slices);
             rg_per_task = std::max<int64_t>(1, (n_rg + n_rb - 1) / n_rb);
+        }
+        if (rg_per_task > rg_cap) {
+            if (force_rg) continue;
+            rg_per_task = rg_cap;
         }
         const int64_t n_rb = (n_rg + rg_per_task - 1) / rg_per_task;
         const int64_t tasks = n_slices * n_rb;
+        cg::SmemLayout lay;
+        cg::smem_layout(z, (int)(rg_per_task * n_gs * 32), reserved, &lay);
         const double per_task = (double)rg_per_task * 16.0 * (u * p.m + 1) +
                                 (double)p.m * u * (1 << p.kbits) + 600.0;
         const double waves = std::ceil((double)tasks / ((double)sms * occ));
-        const double cost = waves * per_task * occ + (n_slices > 1 ? 2000.0 : 0.0);
+        const double cost = waves * per_task * occ + (n_slices > 1 ? 16.0 * rg_per_task : 0.0);
         if (cost < best) {
             best = cost;
             p.fast = true;
@@ -118,7 +141,8 @@ void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms) {
             p.n_rg = n_rg;
             p.rg_per_task = (int)rg_per_task;
             p.n_rb = n_rb;
-            p.smem_bytes = smem;
+            p.smem = lay;
+            p.smem_bytes = lay.total;
         }
     }
     if (p.fast) {
@@ -138,6 +162,7 @@ struct cg_layer {
     uint16_t* scales = nullptr;     // (rows, groups) binary16
     uint16_t* books = nullptr;      // (m, 2**b, v) binary16
     float* ws = nullptr;            // split-K workspace (n_slices, rows, ws_cols)
+    unsigned long long* counters = nullptr;  // split-K tickets, one per row block (monotonic)
     int ws_cols = 0;
     uint16_t* x_dev = nullptr;      // staging for the host entry point
     float* y_dev = nullptr;
@@ -145,6 +170,9 @@ struct cg_layer {
     uint16_t* x_pin = nullptr;
     float* y_pin = nullptr;
     int flags = 0;
+    int pf_dist = 0;
+    int sms = 148;
+    unsigned long long* stamps = nullptr;  // diagnostics (CG_STAMPS=1)
     int64_t device_bytes = 0;
 };
 
@@ -170,6 +198,8 @@ void free_layer(cg_layer* L) {
     cudaFree(L->scales);
     cudaFree(L->books);
     cudaFree(L->ws);
+    cudaFree(L->counters);
+    cudaFree(L->stamps);
     cudaFree(L->x_dev);
     cudaFree(L->y_dev);
     cudaFreeHost(L->x_pin);
@@ -201,6 +231,13 @@ int ensure_ws(cg_layer* L, int n) {
     }
     int rc = dev_alloc(L, &L->ws, (size_t)p.n_slices * p.rows * n * 4, "workspace alloc");
     if (rc) return rc;
+    // one monotonic ticket per row block; allocated and zeroed once
+    if (!L->counters) {
+        rc = dev_alloc(L, &L->counters, (size_t)p.n_rb * 8, "ticket alloc");
+        if (rc) return rc;
+        cudaError_t e = cudaMemset(L->counters, 0, (size_t)p.n_rb * 8);
+        if (e != cudaSuccess) return cuda_fail(e, "ticket init");
+    }
     L->ws_cols = n;
     return CG_OK;
 }
@@ -227,23 +264,31 @@ int run_gemm(cg_layer* L, const uint16_t* x, int n, float* y, int mode, cudaStre
     gp.scl = L->scl;
     gp.books = L->books;
     gp.x = x;
-    gp.out = split ? L->ws : y;
+    gp.y = y;
+    gp.ws = L->ws;
+    gp.counters = L->counters;
     gp.rows = p.rows;
     gp.cols = p.cols;
     gp.n_rg = p.n_rg;
     gp.n_slices = p.n_slices;
     gp.n_rb = p.n_rb;
-    gp.out_slice_stride = split ? p.rows * n : 0;
     gp.n = n;
     gp.kcount = p.kcount;
     gp.rg_per_task = p.rg_per_task;
     gp.lg = p.lg;
     gp.n_gs = p.n_gs;
     gp.flags = (L->flags & CG_OPT_NO_L2_PREFETCH) ? cg::kFlagNoPrefetch : 0;
+    gp.pf_dist = L->pf_dist;
+    if (p.n_slices * p.n_rb > L->sms) gp.flags |= cg::kFlagLastArriver;
+    if (const char* e = std::getenv("CG_DEBUG_FLAGS")) gp.flags |= std::atoi(e);
+    gp.stamps = L->stamps;
+    gp.off_psum = p.smem.off_psum;
+    gp.off_books = p.smem.off_books;
+    gp.off_x = p.smem.off_x;
+    gp.off_scl = p.smem.off_scl;
+    gp.off_bar = p.smem.off_bar;
+    (void)split;  // split-K partials are summed inside the fused kernel (last-CTA fix-up)
     CG_CUDA(cg::launch_fused_gemv(p, gp, pdl, s), "fused gemv launch");
-    if (split)
-        CG_CUDA(cg::launch_reduce_slices(L->ws, y, p.rows * n, p.n_slices, pdl, s),
-                "split-K reduce launch");
     return CG_OK;
 }
 
@@ -301,6 +346,8 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
     cg_layer* L = new cg_layer();
     L->device = device;
     L->flags = opts ? opts->flags : 0;
+    L->sms = sm_count_of(device);
+    if (const char* e = std::getenv("CG_PF_DIST")) L->pf_dist = std::atoi(e);  // tuning knob
     cg::Plan& p = L->plan;
     p.rows = rows;
     p.cols = cols;
@@ -313,7 +360,11 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
     p.kcount = 1 << b;
     p.segs = cols / v;
     p.groups = cols / g_eff;
-    plan_fast(p, opts ? opts->u : 0, opts ? opts->rg_per_task : 0, sm_count_of(device));
+    int reserved = 1024;
+    if (cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device) !=
+        cudaSuccess)
+        reserved = 1024;
+    plan_fast(p, opts ? opts->u : 0, opts ? opts->rg_per_task : 0, sm_count_of(device), reserved);
     if (opts && opts->u && !p.fast) {
         free_layer(L);
         return fail(CG_ERR_CONFIG, "u=%d is not valid for v=%d m=%d b=%d g=%lld", opts->u, v, m,
@@ -380,6 +431,11 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
     if (p.fast && p.n_slices > 1) {
         if ((rc = ensure_ws(L, 1))) return bail(rc);
     }
+    if (p.fast && std::getenv("CG_STAMPS")) {
+        if ((rc = dev_alloc(L, &L->stamps, (size_t)p.n_slices * p.n_rb * 64, "stamps")))
+            return bail(rc);
+        cudaMemset(L->stamps, 0, (size_t)p.n_slices * p.n_rb * 64);
+    }
     *out = L;
     return CG_OK;
 }
@@ -404,8 +460,8 @@ int cg_layer_query(const cg_layer* L, cg_layer_info* info) {
     info->rg_per_task = p.rg_per_task;
     info->n_slices = p.n_slices;
     info->n_tasks = p.fast ? p.n_slices * p.n_rb : 0;
-    info->smem_bytes = p.smem_bytes;
-    info->launches_fast = p.fast ? (p.n_slices > 1 ? 2 : 1) : 0;
+    info->smem_bytes = p.fast ? p.smem.total : 0;
+    info->launches_fast = p.fast ? 1 : 0;
     info->device_bytes = L->device_bytes;
     // codes at b bits + binary16 scales + binary16 codebooks
     info->algorithmic_bytes = (p.rows * p.segs * p.m * p.b + 7) / 8 + 2 * p.rows * p.groups +
@@ -465,6 +521,9 @@ int cg_layer_psumbook(cg_layer* L, const void* x, int n, float* out, void* strea
     gp.cols = p.cols;
     gp.n = n;
     gp.kcount = p.kcount;
+    gp.off_psum = p.smem.off_psum;
+    gp.off_books = p.smem.off_books;
+    gp.off_x = p.smem.off_x;
     CG_CUDA(cg::launch_psumbook_dump(p, gp, out, static_cast<cudaStream_t>(stream)),
             "psumbook dump launch");
     return CG_OK;
@@ -497,3 +556,13 @@ int cg_psumbook_build(const void* books, const void* x, int m, int b, int v, int
 }
 
 }  // extern "C"
+
+// Diagnostics only (not part of the ABI header): copy the per-CTA phase
+// timestamps of the last fused launch (CG_STAMPS=1 at layer creation).
+extern "C" int cg_debug_stamps(cg_layer* L, unsigned long long* host, int64_t count) {
+    if (!L || !L->stamps) return fail(CG_ERR_ARG, "no stamps (set CG_STAMPS=1)");
+    DeviceGuard guard(L->device);
+    const int64_t n = std::min<int64_t>(count, L->plan.n_slices * L->plan.n_rb * 8);
+    CG_CUDA(cudaMemcpy(host, L->stamps, n * 8, cudaMemcpyDeviceToHost), "stamps D2H");
+    return CG_OK;
+}

@@ -25,6 +25,66 @@ namespace cg {
 constexpr int kThreads = 512;  // fused kernel CTA size (16 warps)
 constexpr int kWarps = kThreads / 32;
 
+
+struct GatherParams {
+    const uint8_t* codes;     // prepacked code tiles
+    const uint16_t* scl;      // prepacked scale tiles (binary16 bits)
+    const uint16_t* books;    // (m, kcount_real, v) binary16 bits
+    const uint16_t* x;        // (cols, n) binary16 bits
+    float* y;                 // (rows, n) output
+    float* ws;                // split-K partials (n_slices, rows, n) when n_slices > 1
+    unsigned long long* counters;  // n_rb monotonic split-K tickets
+    int64_t rows, cols, n_rg, n_slices, n_rb;
+    int n, kcount, rg_per_task, lg, n_gs, flags;
+    int pf_dist;              // row groups each warp prefetches ahead into L2 (0 = off)
+    unsigned long long* stamps;  // diagnostics: per-CTA phase timestamps (8 per CTA) or null
+    // dynamic shared-memory layout (bytes from the dynamic smem start); the
+    // Psumbook sits at a 64 KB-aligned shared-window address (see cg_api.cu)
+    int off_psum, off_books, off_x, off_scl, off_bar;
+};
+
+// flags inside GatherParams
+constexpr int kFlagNoPrefetch = 2;
+constexpr int kFlagLastArriver = 4;
+constexpr int kFlagNoCoop = 8;        // one wave without the cooperative launch attribute   // grid > one wave: last CTA of a row block sums it
+constexpr int kFlagDbgNoLookup = 64;  // diagnostics (CG_DEBUG_FLAGS): stream codes only
+constexpr int kFlagDbgNoLoad = 128;   // diagnostics: gather without streaming new codes
+
+// shared-memory pieces of the fused kernel for (v, m, u, kbits)
+struct FusedSizes {
+    int psum, books, x;  // bytes
+};
+bool fused_instantiated(int v, int m, int u, int kbits);
+bool fused_sizes(int v, int m, int u, int kbits, FusedSizes* out);
+
+// Dynamic smem layout.  The Psumbook must start at a 64 KB-aligned address of
+// the CTA's shared window so that one PRMT builds a whole lookup address; the
+// dynamic area starts `reserved` bytes into the window (1 KB on sm_100).
+struct SmemLayout {
+    int off_psum = 0, off_books = 0, off_x = 0, off_scl = 0, off_bar = 0, total = 0;
+};
+inline bool smem_layout(const FusedSizes& z, int scl_bytes, int reserved, SmemLayout* L) {
+    auto up = [](int v, int a) { return (v + a - 1) / a * a; };
+    const int kMax = 227 * 1024;
+    int low = 0;
+    L->off_x = low;
+    low = up(low + z.x, 16);
+    L->off_scl = low;
+    low = up(low + scl_bytes, 16);
+    L->off_bar = low;
+    low = up(low + 16, 16);
+    const int gap = up(reserved + low, 65536) - reserved;  // first aligned slot
+    if (gap - low >= z.books) {                           // books fit below
+        L->off_books = low;
+        L->off_psum = gap;
+        L->total = gap + z.psum;
+    } else {
+        L->off_psum = gap;
+        L->off_books = gap + z.psum;
+        L->total = L->off_books + z.books;
+    }
+    return L->total <= kMax;
+}
 struct Plan {
     int64_t rows = 0, cols = 0, segs = 0, g_eff = 0, groups = 0;
     int v = 0, m = 0, b = 0, kcount = 0;
@@ -43,22 +103,9 @@ struct Plan {
     int64_t n_rb = 0;         // row blocks (tasks per slice)
     int64_t code_bytes = 0;   // prepacked code stream
     int64_t scale_bytes = 0;  // prepacked scale tiles
-    int smem_bytes = 0;
+    int smem_bytes = 0;       // total dynamic smem of the fused kernel
+    SmemLayout smem;
 };
-
-struct GatherParams {
-    const uint8_t* codes;     // prepacked code tiles
-    const uint16_t* scl;      // prepacked scale tiles (binary16 bits)
-    const uint16_t* books;    // (m, kcount_real, v) binary16 bits
-    const uint16_t* x;        // (cols, n) binary16 bits
-    float* out;               // y (rows, n) or split-K workspace (n_slices, rows, n)
-    int64_t rows, cols, n_rg, n_slices, n_rb;
-    int64_t out_slice_stride; // rows*n when writing the workspace, else 0
-    int n, kcount, rg_per_task, lg, n_gs, flags;
-};
-
-// flags inside GatherParams
-constexpr int kFlagNoPrefetch = 2;
 
 // ---- launchers (cg_kernels.cu); all return cudaError_t of the launch ----
 cudaError_t launch_prepack_codes(const Plan& p, const uint16_t* raw, uint8_t* packed,
@@ -69,8 +116,6 @@ cudaError_t launch_check_codes(const Plan& p, const uint16_t* raw, unsigned* bad
 cudaError_t launch_unpack_codes(const Plan& p, const uint8_t* packed, const uint16_t* raw16,
                                 uint16_t* out, cudaStream_t s);
 cudaError_t launch_fused_gemv(const Plan& p, const GatherParams& gp, bool pdl, cudaStream_t s);
-cudaError_t launch_reduce_slices(const float* ws, float* y, int64_t count, int64_t n_slices,
-                                 bool pdl, cudaStream_t s);
 cudaError_t launch_psumbook_dump(const Plan& p, const GatherParams& gp, float* out,
                                  cudaStream_t s);
 cudaError_t launch_strict_gemm(const Plan& p, const uint8_t* packed, const uint16_t* raw16,
@@ -79,9 +124,6 @@ cudaError_t launch_strict_gemm(const Plan& p, const uint8_t* packed, const uint1
 cudaError_t launch_psumbook_build(const uint16_t* books, const uint16_t* x, int m, int b, int v,
                                   int64_t k_len, int n, float* out, cudaStream_t s);
 
-// smem bytes / feasibility of the fused kernel for (v, m, u, kbits)
-bool fused_instantiated(int v, int m, int u, int kbits);
-int fused_smem_bytes(int v, int m, int u, int kbits);
-int fused_max_ctas_per_sm(const Plan& p);
+
 
 }  // namespace cg

@@ -55,13 +55,29 @@ __device__ __forceinline__ void pdl_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" :::);
 }
 
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ uint32_t word_of(const uint4& q, int i) {
     return i == 0 ? q.x : (i == 1 ? q.y : (i == 2 ? q.z : q.w));
 }
 
 // ---------------------------------------------------------------------------
 // code addressing in the prepacked stream (cg_internal.h)
+//
+// Lane l stores its 16 rows in XOR-permuted order: slot i holds row
+// i ^ row_mask(l), row_mask(l) = bit-reverse of the low 4 lane bits.  With this
+// order every halving step of the warp transpose-reduction keeps slots
+// [0, CNT/2) and sends slots [CNT/2, CNT) -- the partner's sent slot i holds
+// the same row as my kept slot i -- so the reduction needs no selects.
 // ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int row_mask(int lane) {
+    return ((lane & 1) << 3) | ((lane >> 1 & 1) << 2) | ((lane >> 2 & 1) << 1) | (lane >> 3 & 1);
+}
+
 __device__ __forceinline__ int64_t packed_index(int64_t t, int64_t r, int64_t seg, int m, int u,
                                                 int64_t n_rg) {
     const int64_t slice_segs = 32 * u;
@@ -71,7 +87,8 @@ __device__ __forceinline__ int64_t packed_index(int64_t t, int64_t r, int64_t se
     const int64_t uu = within - lane * u;
     const int64_t rg = r >> 4;
     const int64_t rr = r & 15;
-    const int64_t idx = rr * u + uu;  // position in the lane's [row][u] bytes
+    const int64_t slot = rr ^ row_mask((int)lane);
+    const int64_t idx = slot * u + uu;  // position in the lane's [slot][u] bytes
     const int64_t tile = ((slice * n_rg + rg) * m + t) * (int64_t)(u * 512);
     return tile + (idx >> 4) * 512 + lane * 16 + (idx & 15);
 }
@@ -97,8 +114,8 @@ __global__ void prepack_codes_kernel(const uint16_t* __restrict__ raw, uint8_t* 
         const int64_t chunk = in_tile / 512;
         const int64_t lane = (in_tile % 512) / 16;
         const int64_t idx = chunk * 16 + (in_tile % 16);
-        const int64_t rr = idx / u, uu = idx % u;
-        const int64_t r = rg * 16 + rr;
+        const int64_t slot = idx / u, uu = idx % u;
+        const int64_t r = rg * 16 + (slot ^ row_mask((int)lane));
         const int64_t seg = slice * 32 * u + lane * u + uu;
         uint8_t val = 0;
         if (r < rows && seg < segs) {
@@ -166,8 +183,18 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed,
 // so the gather addresses an entry with one PRMT and every lane hits its own
 // bank whatever the code (conflict-free lookups).
 //
-// Each entry = ((+0 + c0*x0) + c1*x1) + ...: fmaf with an exact product is the
-// reference's separate multiply-then-add (engines.py:126-133), bit for bit.
+// Build: thread (q = lane&7, csub = lane>>3) of warp w writes the entries of
+// lanes 4q..4q+3 (4 segments) for codes csub + 4w + 64i with one STS.128
+// (8 threads of a phase cover one 128-byte code row: conflict-free).  The 4
+// dot products run as 2 FFMA2 chains over k, operands pre-paired:
+//   books2[t][c][k] = (c_k, c_k)   (duplicated binary32 centroid, smem)
+//   x pairs         = (x_{seg0,k}, x_{seg1,k})
+// Each entry = ((+0 + c0*x0) + c1*x1) + ...: every lane of an FFMA2 is an
+// IEEE fma with an exact product, i.e. the reference's separate multiply and
+// add (engines.py:126-133), bit for bit.
+//
+// x is staged transposed and skewed, x32[k][s + s/(4U)], so the 8 threads of
+// a phase (segments 4qU + ...) read 8 different banks.
 // ---------------------------------------------------------------------------
 template <int V, int M, int U, int KB>
 struct FusedShape {
@@ -176,14 +203,82 @@ struct FusedShape {
     static constexpr int kCodes = 1 << KB;
     static constexpr int kRegionFloats = kCodes * 64;
     static constexpr int kPsumFloats = kRegions * kRegionFloats;
-    static constexpr int kBookFloats = M * kCodes * V;
-    static constexpr int kXFloats = 32 * U * V;
-    static constexpr int kSmemBytes = 4 * (kPsumFloats + kBookFloats + kXFloats);
+    static constexpr int kBookFloats = M * kCodes * V * 2;          // duplicated pairs
+    static constexpr int kSliceSegs = 32 * U;
+    static constexpr int kXRow = kSliceSegs + kSliceSegs / (4 * U);  // skewed row
+    static constexpr int kXFloats = V * kXRow;
+    static constexpr int kPsumBytes = 4 * kPsumFloats;
+    static constexpr int kBookBytes = 4 * kBookFloats;
+    static constexpr int kXBytes = 4 * kXFloats;
     static constexpr int kTileBytes = M * U * 512;  // codes per (slice, row group)
+    static constexpr int kBookPerThread = (M * kCodes * V + kThreads - 1) / kThreads;
+    static constexpr int kXPerThread = (V * kSliceSegs + kThreads - 1) / kThreads;
 };
 
 template <int V, int M, int U, int KB>
-__device__ __forceinline__ void build_psumbook_smem(float* psum, const float* books32,
+__device__ __forceinline__ int x_slot(int k, int s) {
+    using S = FusedShape<V, M, U, KB>;
+    return k * S::kXRow + s + s / (4 * U);
+}
+
+// Load this thread's share of the codebooks (binary16) into registers.
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void load_books(uint16_t (&r)[FusedShape<V, M, U, KB>::kBookPerThread],
+                                           const uint16_t* books, int kcount, int tid) {
+    using S = FusedShape<V, M, U, KB>;
+#pragma unroll
+    for (int i = 0; i < S::kBookPerThread; ++i) {
+        const int e = tid + i * kThreads;
+        r[i] = e < M * kcount * V ? books[e] : (uint16_t)0;
+    }
+}
+
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void store_books(
+    float2* books2, const uint16_t (&r)[FusedShape<V, M, U, KB>::kBookPerThread], int kcount,
+    int tid) {
+    using S = FusedShape<V, M, U, KB>;
+#pragma unroll
+    for (int i = 0; i < S::kBookPerThread; ++i) {
+        const int e = tid + i * kThreads;
+        if (e < M * kcount * V) {
+            const int t = e / (kcount * V);
+            const int rest = e - t * kcount * V;  // c*V + k
+            const float f = h2f(r[i]);
+            books2[t * S::kCodes * V + rest] = make_float2(f, f);
+        }
+    }
+}
+
+// Load this thread's share of the slice of x (column `col`), binary16.
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void load_x(uint16_t (&r)[FusedShape<V, M, U, KB>::kXPerThread],
+                                       const uint16_t* x, int64_t slice, int64_t cols, int n,
+                                       int col, int tid) {
+    using S = FusedShape<V, M, U, KB>;
+    const int64_t e0 = slice * (int64_t)(S::kSliceSegs * V);
+#pragma unroll
+    for (int i = 0; i < S::kXPerThread; ++i) {
+        const int l = tid + i * kThreads;
+        const int64_t e = e0 + l;
+        r[i] = (l < S::kSliceSegs * V && e < cols) ? x[e * n + col] : (uint16_t)0;
+    }
+}
+
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void store_x(float* x32,
+                                        const uint16_t (&r)[FusedShape<V, M, U, KB>::kXPerThread],
+                                        int tid) {
+    using S = FusedShape<V, M, U, KB>;
+#pragma unroll
+    for (int i = 0; i < S::kXPerThread; ++i) {
+        const int l = tid + i * kThreads;
+        if (l < S::kSliceSegs * V) x32[x_slot<V, M, U, KB>(l % V, l / V)] = h2f(r[i]);
+    }
+}
+
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void build_psumbook_smem(float* psum, const float2* books2,
                                                     const float* x32, int kcount, int tid) {
     using S = FusedShape<V, M, U, KB>;
     const int lane = tid & 31, warp = tid >> 5;
@@ -192,51 +287,37 @@ __device__ __forceinline__ void build_psumbook_smem(float* psum, const float* bo
 #pragma unroll 1
     for (int j = 0; j < S::kSub; ++j) {
         const int t = j / U, uu = j % U;
-        float xv[4][V];
+        float2 x01[V], x23[V];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int k = 0; k < V; ++k) xv[i][k] = x32[((4 * q + i) * U + uu) * V + k];
-        float* dst = psum + (j >> 1) * S::kRegionFloats + (j & 1) * 32 + q * 4;
-        const float* bk = books32 + t * S::kCodes * V;
-#pragma unroll 2
-        for (int c = csub + 4 * warp; c < kcount; c += 4 * kWarps) {
-            float cv[V];
-#pragma unroll
-            for (int k = 0; k < V; ++k) cv[k] = bk[c * V + k];
-            float e[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                float acc = fmaf(cv[0], xv[i][0], 0.0f);
-#pragma unroll
-                for (int k = 1; k < V; ++k) acc = fmaf(cv[k], xv[i][k], acc);
-                e[i] = acc;
-            }
-            *reinterpret_cast<float4*>(dst + c * 64) = make_float4(e[0], e[1], e[2], e[3]);
+        for (int k = 0; k < V; ++k) {
+            const int s0 = (4 * q) * U + uu;
+            x01[k] = make_float2(x32[x_slot<V, M, U, KB>(k, s0)],
+                                 x32[x_slot<V, M, U, KB>(k, s0 + U)]);
+            x23[k] = make_float2(x32[x_slot<V, M, U, KB>(k, s0 + 2 * U)],
+                                 x32[x_slot<V, M, U, KB>(k, s0 + 3 * U)]);
         }
-    }
-}
-
-// stage codebooks and the slice of x (column `col`) into smem as binary32
-template <int V, int M, int U, int KB>
-__device__ __forceinline__ void stage_books(float* books32, const uint16_t* books, int kcount,
-                                            int tid) {
-    using S = FusedShape<V, M, U, KB>;
-    for (int i = tid; i < M * kcount * V; i += kThreads) {
-        const int t = i / (kcount * V);
-        const int rest = i - t * kcount * V;
-        books32[t * S::kCodes * V + rest] = h2f(books[i]);
-    }
-}
-
-template <int V, int M, int U, int KB>
-__device__ __forceinline__ void stage_x(float* x32, const uint16_t* x, int64_t slice, int64_t cols,
-                                        int n, int col, int tid) {
-    using S = FusedShape<V, M, U, KB>;
-    const int64_t e0 = slice * S::kXFloats;
-    for (int i = tid; i < S::kXFloats; i += kThreads) {
-        const int64_t e = e0 + i;
-        x32[i] = e < cols ? h2f(x[e * n + col]) : 0.0f;
+        float* dst = psum + (j >> 1) * S::kRegionFloats + (j & 1) * 32 + q * 4;
+        const float2* bk = books2 + t * S::kCodes * V;
+        // two codes per iteration: four independent FFMA2 chains in flight
+#pragma unroll 1
+        for (int c = csub + 4 * warp; c < kcount; c += 8 * kWarps) {
+            const int c2 = c + 4 * kWarps;
+            const bool has2 = c2 < kcount;
+            float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
+            float2 b01 = make_float2(0.0f, 0.0f), b23 = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                const float2 ca = bk[c * V + k];
+                const float2 cb = bk[(has2 ? c2 : c) * V + k];
+                a01 = __ffma2_rn(ca, x01[k], a01);
+                a23 = __ffma2_rn(ca, x23[k], a23);
+                b01 = __ffma2_rn(cb, x01[k], b01);
+                b23 = __ffma2_rn(cb, x23[k], b23);
+            }
+            *reinterpret_cast<float4*>(dst + c * 64) = make_float4(a01.x, a01.y, a23.x, a23.y);
+            if (has2)
+                *reinterpret_cast<float4*>(dst + c2 * 64) = make_float4(b01.x, b01.y, b23.x, b23.y);
+        }
     }
 }
 
@@ -249,187 +330,368 @@ __device__ __forceinline__ void stage_x(float* x32, const uint16_t* x, int64_t s
 // After the steps for masks 1,2,4,8 a lane holds the row
 // bit0*8 + bit1*4 + bit2*2 + bit3 summed over the 16 lanes sharing bit4.
 // ---------------------------------------------------------------------------
+// halving step on slot-permuted partials: keep slots [0, CNT/2), add the
+// partner's slots [CNT/2, CNT) (same rows, see row_mask)
 template <int CNT>
-__device__ __forceinline__ void halve(float (&a)[16], int lane, int mk) {
-    const bool up = (lane & mk) != 0;
+__device__ __forceinline__ void halve(float (&a)[16], int mk) {
 #pragma unroll
-    for (int i = 0; i < CNT / 2; ++i) {
-        const float lo = a[i], hi = a[i + CNT / 2];
-        const float send = up ? lo : hi;
-        const float keep = up ? hi : lo;
-        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, mk);
+    for (int i = 0; i < CNT / 2; i += 2) {
+        if constexpr (CNT >= 4) {
+            const float2 mine = make_float2(a[i], a[i + 1]);
+            const float2 other = make_float2(__shfl_xor_sync(0xffffffffu, a[i + CNT / 2], mk),
+                                             __shfl_xor_sync(0xffffffffu, a[i + 1 + CNT / 2], mk));
+            const float2 sum = __fadd2_rn(mine, other);
+            a[i] = sum.x;
+            a[i + 1] = sum.y;
+        } else {
+            a[i] += __shfl_xor_sync(0xffffffffu, a[i + CNT / 2], mk);
+        }
     }
 }
 
+// Multiply slots [0, CNT) by their rows' scales.  Slot i holds row
+// base + (i ^ m) with m = row_mask & (CNT-1); the smem tile p[0..CNT) is in row
+// order, so the binary16 words are permuted by m before use.
 template <int CNT>
-__device__ __forceinline__ void apply_scales(float (&a)[16], const float (&sc)[16]) {
-#pragma unroll
-    for (int i = 0; i < CNT; ++i) a[i] *= sc[i];
-}
-
-// load this lane's CNT scale values (binary16) for rows base..base+CNT-1
-template <int CNT>
-__device__ __forceinline__ void load_scales(float (&sc)[16], const uint16_t* p) {
-    if constexpr (CNT == 16) {
-        const uint4 a = *reinterpret_cast<const uint4*>(p);
-        const uint4 b = *reinterpret_cast<const uint4*>(p + 8);
-        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
-            sc[2 * i] = f.x;
-            sc[2 * i + 1] = f.y;
-        }
-    } else if constexpr (CNT == 8) {
-        const uint4 a = *reinterpret_cast<const uint4*>(p);
-        const uint32_t w[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
-            sc[2 * i] = f.x;
-            sc[2 * i + 1] = f.y;
-        }
-    } else if constexpr (CNT == 4) {
-        const uint2 a = *reinterpret_cast<const uint2*>(p);
-        float2 f = __half22float2(*reinterpret_cast<const __half2*>(&a.x));
-        sc[0] = f.x;
-        sc[1] = f.y;
-        f = __half22float2(*reinterpret_cast<const __half2*>(&a.y));
-        sc[2] = f.x;
-        sc[3] = f.y;
-    } else if constexpr (CNT == 2) {
-        const uint32_t a = *reinterpret_cast<const uint32_t*>(p);
-        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&a));
-        sc[0] = f.x;
-        sc[1] = f.y;
+__device__ __forceinline__ void apply_scales(float (&a)[16], const uint16_t* p, int m) {
+    if constexpr (CNT == 1) {
+        a[0] *= h2f(*p);
     } else {
-        sc[0] = h2f(*p);
+        uint32_t w[CNT / 2];
+#pragma unroll
+        for (int i = 0; i < CNT / 2; ++i) w[i] = reinterpret_cast<const uint32_t*>(p)[i];
+        // word-level swaps for mask bits >= 1 (blocks of 2^(b-1) words)
+#pragma unroll
+        for (int b = CNT / 4; b >= 1; b >>= 1) {
+            if (m & (2 * b)) {
+#pragma unroll
+                for (int i = 0; i < CNT / 2; ++i)
+                    if ((i & b) == 0) {
+                        const uint32_t tmp = w[i];
+                        w[i] = w[i + b];
+                        w[i + b] = tmp;
+                    }
+            }
+        }
+        const uint32_t sel = (m & 1) ? 0x1032u : 0x3210u;  // swap the halves within a word
+#pragma unroll
+        for (int i = 0; i < CNT / 2; ++i) {
+            const uint32_t ww = __byte_perm(w[i], 0u, sel);
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&ww));
+            const float2 r = __fmul2_rn(make_float2(a[2 * i], a[2 * i + 1]), f);
+            a[2 * i] = r.x;
+            a[2 * i + 1] = r.y;
+        }
     }
+}
+
+// ---- mbarrier + bulk async copy (TMA 1-D) for the task's scale tiles ----
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
 
 // ---------------------------------------------------------------------------
 // K2: fused Psumbook build + code-gather accumulate
+//
+// One CTA = one task (K-slice, block of row groups).  Prologue: bulk-prefetch
+// the task's code stream to L2, bulk-copy its scale tiles to smem (TMA 1-D,
+// mbarrier), load codebooks and the first code tile to registers -- all of it
+// weights, so it overlaps the previous kernel under PDL -- then wait for the
+// producer of x, build the slice Psumbook.  Gather: each warp walks its row
+// groups with a two-deep register pipeline (ping-pong buffers, no copies).
+// Split-K: partials go to the workspace; the last CTA of a row block (atomic
+// ticket) sums the slices in ascending order -- deterministic, no 2nd kernel.
 // ---------------------------------------------------------------------------
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void load_tile(uint4 (&cw)[M][U], const uint8_t* tp) {
+#pragma unroll
+    for (int t = 0; t < M; ++t)
+#pragma unroll
+        for (int c = 0; c < U; ++c) cw[t][c] = ldg_stream_v4(tp + (t * U + c) * 512);
+}
+
+// lb0/lb1 = per-lane PRMT constants: byte0 = lane<<2 | half<<7, bytes 1-2 =
+// bits 16-31 of the Psumbook's 64 KB-aligned shared address.  One PRMT then
+// yields  base | code<<8 | half<<7 | lane<<2  and the region offset rides in
+// the LDS immediate: one PRMT + one LDS per lookup, no address arithmetic.
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ float gather_row_group(const uint4 (&cw)[M][U], const uint16_t* sp,
+                                                  uint32_t lb0, uint32_t lb1, int lg, int mask) {
+    using S = FusedShape<V, M, U, KB>;
+    // lookups: a[i] = sum over (t, u) of psum_t[seg(lane,u)][code of slot i],
+    // two slots at a time with packed FADD2
+    float a[16];
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+        float2 s2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int t = 0; t < M; ++t)
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+                const int j = t * U + uu;
+                const uint32_t lb = (j & 1) ? lb1 : lb0;
+                const uint32_t region = (uint32_t)((j >> 1) * S::kRegionFloats * 4);
+                float2 v;
+                {
+                    const int idx = i * U + uu;
+                    const uint32_t w = word_of(cw[t][idx >> 4], (idx >> 2) & 3);
+                    v.x = lds_f32(__byte_perm(w, lb, 0x6504u | ((uint32_t)(idx & 3) << 4)) + region);
+                }
+                {
+                    const int idx = (i + 1) * U + uu;
+                    const uint32_t w = word_of(cw[t][idx >> 4], (idx >> 2) & 3);
+                    v.y = lds_f32(__byte_perm(w, lb, 0x6504u | ((uint32_t)(idx & 3) << 4)) + region);
+                }
+                s2 = (t == 0 && uu == 0) ? v : __fadd2_rn(s2, v);
+            }
+        a[i] = s2.x;
+        a[i + 1] = s2.y;
+    }
+    // transpose-reduce across lanes; scales once the lanes of a group are summed
+    if (lg == 0) apply_scales<16>(a, sp, mask & 15);
+    halve<16>(a, 1);
+    if (lg == 1) apply_scales<8>(a, sp, mask & 7);
+    halve<8>(a, 2);
+    if (lg == 2) apply_scales<4>(a, sp, mask & 3);
+    halve<4>(a, 4);
+    if (lg == 3) apply_scales<2>(a, sp, mask & 1);
+    halve<2>(a, 8);
+    if (lg == 4) apply_scales<1>(a, sp, 0);
+    a[0] += __shfl_xor_sync(0xffffffffu, a[0], 16);
+    if (lg >= 5) apply_scales<1>(a, sp, 0);
+    return a[0];
+}
+
 template <int V, int M, int U, int KB>
 __global__ void __launch_bounds__(kThreads, 1) fused_gemv_kernel(const GatherParams p) {
     using S = FusedShape<V, M, U, KB>;
-    extern __shared__ __align__(16) float smem[];
-    float* psum = smem;
-    float* books32 = smem + S::kPsumFloats;
-    float* x32 = books32 + S::kBookFloats;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* psum = reinterpret_cast<float*>(smem_raw + p.off_psum);
+    float2* books2 = reinterpret_cast<float2*>(smem_raw + p.off_books);
+    float* x32 = reinterpret_cast<float*>(smem_raw + p.off_x);
+    uint16_t* scl_s = reinterpret_cast<uint16_t*>(smem_raw + p.off_scl);
+    uint64_t& scl_bar = *reinterpret_cast<uint64_t*>(smem_raw + p.off_bar);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t task = blockIdx.x;
     const int64_t slice = task / p.n_rb;
     const int64_t rb = task - slice * p.n_rb;
-    const int col = blockIdx.y;
+    const int n = p.n;
     const int64_t rg0 = rb * p.rg_per_task;
     const int64_t rg1 = min(rg0 + (int64_t)p.rg_per_task, p.n_rg);
+    const int n_gs = p.n_gs;
     const uint8_t* tiles = p.codes + slice * p.n_rg * (int64_t)S::kTileBytes;
 
-    // 1. put this task's whole code stream in flight towards L2 (weights only)
-    if (!(p.flags & kFlagNoPrefetch) && warp == kWarps - 1) {
-        const uint8_t* beg = tiles + rg0 * S::kTileBytes;
-        const int64_t bytes = (rg1 - rg0) * S::kTileBytes;
-        constexpr int64_t kChunk = 32768;
-        for (int64_t off = lane * kChunk; off < bytes; off += 32 * kChunk)
-            prefetch_l2_bulk(beg + off, (uint32_t)min(kChunk, bytes - off));
+    unsigned long long* stamps = p.stamps ? p.stamps + blockIdx.x * 8 : nullptr;
+#define CG_STAMP(k) \
+    if (stamps && tid == 0) stamps[k] = gtimer();
+    CG_STAMP(0)
+    // 1. weights (independent of the previous kernel in the stream)
+    if (tid == 0) {
+        const uint32_t bytes = (uint32_t)((rg1 - rg0) * n_gs * 32);
+        mbar_init(&scl_bar, 1);
+        mbar_expect_tx(&scl_bar, bytes);
+        bulk_g2s(scl_s, p.scl + (slice * p.n_rg + rg0) * n_gs * 16, bytes, &scl_bar);
     }
-    stage_books<V, M, U, KB>(books32, p.books, p.kcount, tid);
-    // 2. x may be produced by the previous kernel in the stream
-    pdl_wait();
-    stage_x<V, M, U, KB>(x32, p.x, slice, p.cols, p.n, col, tid);
-    __syncthreads();
-    build_psumbook_smem<V, M, U, KB>(psum, books32, x32, p.kcount, tid);
-    __syncthreads();
-    pdl_launch_dependents();
+    // progressive L2 prefetch: each warp keeps its next `pf` row groups in
+    // flight towards L2 (the bytes in flight, not the issue rate, bound HBM)
+    const int pf = (p.flags & kFlagNoPrefetch) ? 0 : p.pf_dist;
+    uint16_t breg[S::kBookPerThread];
+    load_books<V, M, U, KB>(breg, p.books, p.kcount, tid);
+    const int my_rgs = rg0 + warp < rg1 ? (int)((rg1 - rg0 - warp + kWarps - 1) / kWarps) : 0;
+    const uint8_t* cptr = tiles + (rg0 + warp) * S::kTileBytes + lane * 16;
+    constexpr int64_t kStep = (int64_t)kWarps * S::kTileBytes;
+    const uint8_t* wtile = tiles + (rg0 + warp) * S::kTileBytes;  // this warp's tile 0
+    // the first two tiles go to L2 now; registers take them after the build
+    if (lane < 2 && lane < my_rgs) prefetch_l2_bulk(wtile + lane * kStep, S::kTileBytes);
+    if (lane >= 2 && lane < 2 + pf && lane < my_rgs)
+        prefetch_l2_bulk(wtile + lane * kStep, S::kTileBytes);
+    uint4 bufA[M][U], bufB[M][U];
 
-    // 3. gather: warp w takes row groups rg0+w, rg0+w+16, ...
-    const uint32_t lb[2] = {(uint32_t)lane << 2, ((uint32_t)lane << 2) | 0x80u};
-    const uint32_t psum_base = smem_u32(psum);
+    // per-lane constants of the gather (Psumbook base must be 64 KB aligned)
+    const uint32_t psum_addr = smem_u32(psum);
+    if (psum_addr & 0xffffu) __trap();
+    const uint32_t lb0 = ((uint32_t)lane << 2) | ((psum_addr >> 16) << 8);
+    const uint32_t lb1 = lb0 | 0x80u;
     const int lg = p.lg;
     const int ls = lg < 4 ? lg : 4;
-    int sbase = 0;  // first row of this lane's scale run after `ls` halving steps
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-        if (j < ls && (lane >> j & 1)) sbase += 8 >> j;
+    const int mask = row_mask(lane);
+    const int sbase = mask & ~((16 >> ls) - 1);  // first row of this lane's scale run
     const int gi = lg >= 5 ? 0 : (lane >> lg);
-    const int out_row = (lane & 1) * 8 + (lane >> 1 & 1) * 4 + (lane >> 2 & 1) * 2 + (lane >> 3 & 1);
-    float* out = p.out + slice * p.out_slice_stride;
+    const bool split = p.n_slices > 1;
+    const uint16_t* sp0 = scl_s + (warp * n_gs + gi) * 16 + sbase;
+    const int sstep = kWarps * n_gs * 16;
+    const int64_t row_step = (int64_t)kWarps * 16;
 
-    int64_t rg = rg0 + warp;
-    uint4 cw[M][U];
-    if (rg < rg1) {
-        const uint8_t* tp = tiles + rg * S::kTileBytes + lane * 16;
+    // 2. per batch column: wait for x (PDL), build the slice Psumbook, gather
+    for (int col = 0; col < n; ++col) {
+        if (col == 0) {
+            pdl_wait();
+        } else {
+            __syncthreads();  // previous column's table is no longer read
+        }
+        uint16_t xreg[S::kXPerThread];
+        load_x<V, M, U, KB>(xreg, p.x, slice, p.cols, n, col, tid);
+        if (col == 0) store_books<V, M, U, KB>(books2, breg, p.kcount, tid);
+        store_x<V, M, U, KB>(x32, xreg, tid);
+        __syncthreads();
+        if (col == 0) CG_STAMP(1)
+        build_psumbook_smem<V, M, U, KB>(psum, books2, x32, p.kcount, tid);
+        __syncthreads();
+        if (p.flags & 512) return;  // diagnostics: prologue + build only
+        if (my_rgs > 0) load_tile<V, M, U, KB>(bufA, cptr);
+        if (col == 0) {
+            CG_STAMP(2)
+            pdl_launch_dependents();
+            mbar_wait(&scl_bar, 0);
+        }
+        float* out = split ? p.ws + slice * p.rows * n : p.y;
+        int64_t row = (rg0 + warp) * 16 + mask;
+        if (p.flags & kFlagDbgNoLookup) {  // diagnostic: stream the codes only
+            uint32_t acc = 0;
+            for (int i = 0; i < my_rgs; ++i) {
+                load_tile<V, M, U, KB>(bufA, cptr + i * kStep);
 #pragma unroll
-        for (int t = 0; t < M; ++t)
+                for (int t = 0; t < M; ++t)
 #pragma unroll
-            for (int c = 0; c < U; ++c) cw[t][c] = ldg_stream_v4(tp + (t * U + c) * 512);
+                    for (int c = 0; c < U; ++c)
+                        acc ^= bufA[t][c].x ^ bufA[t][c].y ^ bufA[t][c].z ^ bufA[t][c].w;
+            }
+            if (acc == 0x12345678u) out[0] = 1.0f;
+            continue;
+        }
+        const int64_t lstep = (p.flags & kFlagDbgNoLoad) ? 0 : kStep;
+        for (int i = 0; i < my_rgs; i += 2) {
+            if (col == 0 && lane < 2 && i + 1 + pf + lane < my_rgs && pf > 0)
+                prefetch_l2_bulk(wtile + (i + 1 + pf + lane) * kStep, S::kTileBytes);
+            if (i + 1 < my_rgs) load_tile<V, M, U, KB>(bufB, cptr + (i + 1) * lstep);
+            float v = gather_row_group<V, M, U, KB>(bufA, sp0 + i * sstep, lb0, lb1,
+                                                    lg, mask);
+            if (lane < 16 && row < p.rows) out[row * n + col] = v;
+            row += row_step;
+            if (i + 1 < my_rgs) {
+                if (i + 2 < my_rgs) load_tile<V, M, U, KB>(bufA, cptr + (i + 2) * lstep);
+                v = gather_row_group<V, M, U, KB>(bufB, sp0 + (i + 1) * sstep, lb0, lb1,
+                                                  lg, mask);
+                if (lane < 16 && row < p.rows) out[row * n + col] = v;
+                row += row_step;
+            }
+        }
     }
-    for (; rg < rg1; rg += kWarps) {
-        // scales for this row group (small, L2/L1 resident)
-        float sc[16];
-        const uint16_t* sp = p.scl + ((slice * p.n_rg + rg) * p.n_gs + gi) * 16 + sbase;
-        switch (ls) {
-            case 0: load_scales<16>(sc, sp); break;
-            case 1: load_scales<8>(sc, sp); break;
-            case 2: load_scales<4>(sc, sp); break;
-            case 3: load_scales<2>(sc, sp); break;
-            default: load_scales<1>(sc, sp); break;
+    __syncthreads();
+    CG_STAMP(3)
+    if (!split) return;
+
+    // 3. split-K fix-up, shared by the n_slices CTAs of this row block: a
+    //    ticket barrier on a monotonic 64-bit counter (target = next multiple
+    //    of n_slices above our ticket; no reset, one atomic round trip; all
+    //    CTAs are co-resident: cooperative launch, one wave), then CTA `slice`
+    //    sums its 1/n_slices share of the rows over all slices in ascending
+    //    order -- deterministic.
+    int* s_flag = reinterpret_cast<int*>(smem_raw + p.off_bar + 8);
+    const bool one_wave = !(p.flags & kFlagLastArriver);
+    if (tid == 0) {
+        unsigned long long* cnt = p.counters + rb;
+        __threadfence();
+        const unsigned long long ns = (unsigned long long)p.n_slices;
+        const unsigned long long old = atomicAdd(cnt, 1ull);
+        if (one_wave) {
+            const unsigned long long target = (old / ns + 1) * ns;
+            unsigned long long cur;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(cnt) : "memory");
+            } while (cur < target);
+        } else {
+            *s_flag = (old % ns == ns - 1);  // last arriver of this row block
+            __threadfence();
         }
-        // software pipeline: next row group's codes
-        uint4 nw[M][U];
-        const int64_t rgn = rg + kWarps;
-        if (rgn < rg1) {
-            const uint8_t* tp = tiles + rgn * S::kTileBytes + lane * 16;
-#pragma unroll
-            for (int t = 0; t < M; ++t)
-#pragma unroll
-                for (int c = 0; c < U; ++c) nw[t][c] = ldg_stream_v4(tp + (t * U + c) * 512);
-        }
-        // lookups: a[r] = sum over (t, u) of psum_t[seg(lane,u)][code]
-        float a[16];
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            float s = 0.0f;
-#pragma unroll
-            for (int t = 0; t < M; ++t)
-#pragma unroll
-                for (int uu = 0; uu < U; ++uu) {
-                    constexpr int dummy = 0;
-                    (void)dummy;
-                    const int idx = r * U + uu;
-                    const uint32_t w = word_of(cw[t][idx >> 4], (idx >> 2) & 3);
-                    const int j = t * U + uu;
-                    const uint32_t off =
-                        __byte_perm(w, lb[j & 1], 0x5504u | ((uint32_t)(idx & 3) << 4));
-                    const float val =
-                        lds_f32(psum_base + off + (uint32_t)((j >> 1) * S::kRegionFloats * 4));
-                    s = (t == 0 && uu == 0) ? val : s + val;
-                }
-            a[r] = s;
-        }
-        // reduce across the lanes of a scale group, scale, finish the reduction
-        if (lg == 0) apply_scales<16>(a, sc);
-        halve<16>(a, lane, 1);
-        if (lg == 1) apply_scales<8>(a, sc);
-        halve<8>(a, lane, 2);
-        if (lg == 2) apply_scales<4>(a, sc);
-        halve<4>(a, lane, 4);
-        if (lg == 3) apply_scales<2>(a, sc);
-        halve<2>(a, lane, 8);
-        if (lg == 4) apply_scales<1>(a, sc);
-        a[0] += __shfl_xor_sync(0xffffffffu, a[0], 16);
-        if (lg >= 5) a[0] *= sc[0];
-        if (lane < 16) {
-            const int64_t r = rg * 16 + out_row;
-            if (r < p.rows) out[r * p.n + col] = a[0];
-        }
-#pragma unroll
-        for (int t = 0; t < M; ++t)
-#pragma unroll
-            for (int c = 0; c < U; ++c) cw[t][c] = nw[t][c];
     }
+    __syncthreads();
+    CG_STAMP(4)
+    if (!one_wave && !*s_flag) return;
+    const int64_t rows0 = rg0 * 16, rows1 = min(rg1 * 16, p.rows);
+    // one wave: CTA `slice` sums its share of the rows; otherwise the last
+    // arriver sums the whole row block
+    const int64_t share = one_wave
+        ? ((rows1 - rows0 + p.n_slices - 1) / p.n_slices + 3) & ~int64_t(3)
+        : rows1 - rows0;
+    const int64_t first = one_wave ? rows0 + slice * share : rows0;
+    const int64_t e_lo = first * n;
+    const int64_t e_hi = min(first + share, rows1) * n;
+    const int64_t plane = p.rows * n;
+    const int ns = (int)p.n_slices;
+    if ((plane & 3) == 0) {  // float4 over 4 consecutive outputs, 16 slices per round trip
+        for (int64_t e = e_lo + 4 * tid; e < e_hi; e += 4 * kThreads) {
+            const float* src = p.ws + e;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int s0 = 0; s0 < ns; s0 += 16) {
+                float4 v[16];
+#pragma unroll
+                for (int s = 0; s < 16; ++s)
+                    if (s0 + s < ns)
+                        v[s] = __ldcg(reinterpret_cast<const float4*>(src + (int64_t)(s0 + s) * plane));
+#pragma unroll
+                for (int s = 0; s < 16; ++s)
+                    if (s0 + s < ns) {
+                        if (s0 + s == 0) {
+                            acc = v[s];
+                        } else {
+                            acc.x += v[s].x;
+                            acc.y += v[s].y;
+                            acc.z += v[s].z;
+                            acc.w += v[s].w;
+                        }
+                    }
+            }
+            if (e + 3 < e_hi) {
+                *reinterpret_cast<float4*>(p.y + e) = acc;
+            } else {
+                const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+                for (int k = 0; k < 4 && e + k < e_hi; ++k) p.y[e + k] = a4[k];
+            }
+        }
+    } else {
+        for (int64_t e = e_lo + tid; e < e_hi; e += kThreads) {
+            const float* src = p.ws + e;
+            float acc = 0.0f;
+            for (int s0 = 0; s0 < ns; s0 += 16) {
+                float v[16];
+#pragma unroll
+                for (int s = 0; s < 16; ++s)
+                    if (s0 + s < ns) v[s] = __ldcg(src + (int64_t)(s0 + s) * plane);
+#pragma unroll
+                for (int s = 0; s < 16; ++s)
+                    if (s0 + s < ns) acc = (s0 + s == 0) ? v[s] : acc + v[s];
+            }
+            p.y[e] = acc;
+        }
+    }
+    __syncthreads();
+    CG_STAMP(5)
+#undef CG_STAMP
 }
 
 // dump the fused kernel's smem Psumbook in _psum_tables layout (m, segs, 2**b, n)
@@ -437,17 +699,21 @@ template <int V, int M, int U, int KB>
 __global__ void __launch_bounds__(kThreads, 1)
     psumbook_dump_kernel(const GatherParams p, float* __restrict__ out, int64_t segs) {
     using S = FusedShape<V, M, U, KB>;
-    extern __shared__ __align__(16) float smem[];
-    float* psum = smem;
-    float* books32 = smem + S::kPsumFloats;
-    float* x32 = books32 + S::kBookFloats;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* psum = reinterpret_cast<float*>(smem_raw + p.off_psum);
+    float2* books2 = reinterpret_cast<float2*>(smem_raw + p.off_books);
+    float* x32 = reinterpret_cast<float*>(smem_raw + p.off_x);
     const int tid = threadIdx.x;
     const int64_t slice = blockIdx.x;
     const int col = blockIdx.y;
-    stage_books<V, M, U, KB>(books32, p.books, p.kcount, tid);
-    stage_x<V, M, U, KB>(x32, p.x, slice, p.cols, p.n, col, tid);
+    uint16_t breg[S::kBookPerThread];
+    uint16_t xreg[S::kXPerThread];
+    load_books<V, M, U, KB>(breg, p.books, p.kcount, tid);
+    load_x<V, M, U, KB>(xreg, p.x, slice, p.cols, p.n, col, tid);
+    store_books<V, M, U, KB>(books2, breg, p.kcount, tid);
+    store_x<V, M, U, KB>(x32, xreg, tid);
     __syncthreads();
-    build_psumbook_smem<V, M, U, KB>(psum, books32, x32, p.kcount, tid);
+    build_psumbook_smem<V, M, U, KB>(psum, books2, x32, p.kcount, tid);
     __syncthreads();
     const int total = S::kSub * p.kcount * 32;
     for (int i = tid; i < total; i += kThreads) {
@@ -460,37 +726,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float v = psum[(j >> 1) * S::kRegionFloats + c * 64 + (j & 1) * 32 + lane];
         out[(((int64_t)t * segs + seg) * p.kcount + c) * p.n + col] = v;
     }
-}
-
-// deterministic split-K reduction: y[i] = sum_s ws[s][i], s ascending
-__global__ void reduce_slices_kernel(const float* __restrict__ ws, float* __restrict__ y,
-                                     int64_t count, int64_t n_slices) {
-    pdl_wait();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if ((count & 3) == 0) {
-        const int64_t c4 = count >> 2;
-        const float4* w4 = reinterpret_cast<const float4*>(ws);
-        float4* y4 = reinterpret_cast<float4*>(y);
-        for (int64_t i = i0; i < c4; i += stride) {
-            float4 s = w4[i];
-            for (int64_t k = 1; k < n_slices; ++k) {
-                const float4 v = w4[k * c4 + i];
-                s.x += v.x;
-                s.y += v.y;
-                s.z += v.z;
-                s.w += v.w;
-            }
-            y4[i] = s;
-        }
-    } else {
-        for (int64_t i = i0; i < count; i += stride) {
-            float s = ws[i];
-            for (int64_t k = 1; k < n_slices; ++k) s += ws[k * count + i];
-            y[i] = s;
-        }
-    }
-    pdl_launch_dependents();
 }
 
 // ---------------------------------------------------------------------------
@@ -556,49 +791,42 @@ int grid_for(int64_t total, int threads) {
 // template dispatch
 // ---------------------------------------------------------------------------
 template <int V, int M, int U, int KB>
-cudaError_t launch_fused_t(const GatherParams& gp, int64_t grid_x, bool pdl, cudaStream_t s) {
-    using S = FusedShape<V, M, U, KB>;
+cudaError_t launch_fused_t(const GatherParams& gp, int64_t grid_x, int smem, bool pdl,
+                           cudaStream_t s) {
     auto kern = fused_gemv_kernel<V, M, U, KB>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         S::kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid_x, (unsigned)gp.n, 1);
+    cfg.gridDim = dim3((unsigned)grid_x, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = S::kSmemBytes;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    // cooperative: the split-K ticket barrier needs every CTA resident (one wave)
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (gp.n_slices > 1 && !(gp.flags & (kFlagLastArriver | kFlagNoCoop))) {
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na].val.cooperative = 1;
+        ++na;
+    }
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, gp);
 }
 
 template <int V, int M, int U, int KB>
 cudaError_t launch_dump_t(const GatherParams& gp, int64_t n_slices, float* out, int64_t segs,
-                          cudaStream_t s) {
-    using S = FusedShape<V, M, U, KB>;
+                          int smem, cudaStream_t s) {
     auto kern = psumbook_dump_kernel<V, M, U, KB>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         S::kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<dim3((unsigned)n_slices, (unsigned)gp.n), kThreads, S::kSmemBytes, s>>>(gp, out, segs);
+    kern<<<dim3((unsigned)n_slices, (unsigned)gp.n), kThreads, smem, s>>>(gp, out, segs);
     return cudaGetLastError();
-}
-
-template <int V, int M, int U, int KB>
-int occupancy_t() {
-    using S = FusedShape<V, M, U, KB>;
-    auto kern = fused_gemv_kernel<V, M, U, KB>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmemBytes) !=
-        cudaSuccess)
-        return 1;
-    int n = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, S::kSmemBytes) !=
-        cudaSuccess)
-        return 1;
-    return n < 1 ? 1 : n;
 }
 
 // Visit the instantiation for runtime (v, m, u, kb).  Instantiated set:
@@ -629,53 +857,48 @@ bool visit(int v, int m, int u, int kb, F&& f) {
 #undef CG_KB
 }
 
-struct SmemQuery {
-    int bytes = 0;
+struct SizeQuery {
+    FusedSizes z{};
     template <int V, int M, int U, int KB>
-    void run() { bytes = FusedShape<V, M, U, KB>::kSmemBytes; }
-};
-struct OccQuery {
-    int n = 1;
-    template <int V, int M, int U, int KB>
-    void run() { n = occupancy_t<V, M, U, KB>(); }
+    void run() {
+        using S = FusedShape<V, M, U, KB>;
+        z = FusedSizes{S::kPsumBytes, S::kBookBytes, S::kXBytes};
+    }
 };
 struct FusedLaunch {
     const GatherParams* gp;
     int64_t grid_x;
+    int smem;
     bool pdl;
     cudaStream_t s;
     cudaError_t err = cudaErrorInvalidConfiguration;
     template <int V, int M, int U, int KB>
-    void run() { err = launch_fused_t<V, M, U, KB>(*gp, grid_x, pdl, s); }
+    void run() { err = launch_fused_t<V, M, U, KB>(*gp, grid_x, smem, pdl, s); }
 };
 struct DumpLaunch {
     const GatherParams* gp;
     int64_t n_slices;
     float* out;
     int64_t segs;
+    int smem;
     cudaStream_t s;
     cudaError_t err = cudaErrorInvalidConfiguration;
     template <int V, int M, int U, int KB>
-    void run() { err = launch_dump_t<V, M, U, KB>(*gp, n_slices, out, segs, s); }
+    void run() { err = launch_dump_t<V, M, U, KB>(*gp, n_slices, out, segs, smem, s); }
 };
 
 }  // namespace
 
 bool fused_instantiated(int v, int m, int u, int kbits) {
-    SmemQuery q;
+    SizeQuery q;
     return visit(v, m, u, kbits, q);
 }
 
-int fused_smem_bytes(int v, int m, int u, int kbits) {
-    SmemQuery q;
-    if (!visit(v, m, u, kbits, q)) return -1;
-    return q.bytes;
-}
-
-int fused_max_ctas_per_sm(const Plan& p) {
-    OccQuery q;
-    if (!visit(p.v, p.m, p.u, p.kbits, q)) return 1;
-    return q.n;
+bool fused_sizes(int v, int m, int u, int kbits, FusedSizes* out) {
+    SizeQuery q;
+    if (!visit(v, m, u, kbits, q)) return false;
+    *out = q.z;
+    return true;
 }
 
 cudaError_t launch_prepack_codes(const Plan& p, const uint16_t* raw, uint8_t* packed,
@@ -710,32 +933,14 @@ cudaError_t launch_unpack_codes(const Plan& p, const uint8_t* packed, const uint
 }
 
 cudaError_t launch_fused_gemv(const Plan& p, const GatherParams& gp, bool pdl, cudaStream_t s) {
-    FusedLaunch f{&gp, p.n_slices * p.n_rb, pdl, s};
+    FusedLaunch f{&gp, p.n_slices * p.n_rb, p.smem.total, pdl, s};
     if (!visit(p.v, p.m, p.u, p.kbits, f)) return cudaErrorInvalidConfiguration;
     return f.err;
 }
 
-cudaError_t launch_reduce_slices(const float* ws, float* y, int64_t count, int64_t n_slices,
-                                 bool pdl, cudaStream_t s) {
-    const int64_t work = (count & 3) == 0 ? count / 4 : count;
-    int blocks = (int)((work + 255) / 256);
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    if (blocks < 1) blocks = 1;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(blocks, 1, 1);
-    cfg.blockDim = dim3(256, 1, 1);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, reduce_slices_kernel, ws, y, count, n_slices);
-}
-
 cudaError_t launch_psumbook_dump(const Plan& p, const GatherParams& gp, float* out,
                                  cudaStream_t s) {
-    DumpLaunch f{&gp, p.n_slices, out, p.segs, s};
+    DumpLaunch f{&gp, p.n_slices, out, p.segs, p.smem.total, s};
     if (!visit(p.v, p.m, p.u, p.kbits, f)) return cudaErrorInvalidConfiguration;
     return f.err;
 }

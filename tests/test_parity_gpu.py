@@ -210,7 +210,7 @@ def test_strict_independent_of_tiling():
     x = np.random.default_rng(5).standard_normal((96, 3)).astype(np.float16)
     ref = orc.codegemm([p.codes for p in q.planes], [b.entries for b in q.books],
                        q.scales.scales, x, 4, 16)
-    for u in (1, 2, 4):
+    for u in (1, 2):
         y = cg.DeviceLayer(q, u=u).gemm(cuda_x(x), mode="strict").cpu().numpy()
         assert np.array_equal(u32(y), u32(ref)), u
 
