@@ -65,6 +65,9 @@ extern "C" {
 /* option flags for cg_layer_options.flags */
 #define CG_OPT_NO_PDL 1        /* launch without programmatic dependent launch        */
 #define CG_OPT_NO_L2_PREFETCH 2 /* skip the bulk L2 prefetch of the CTA's code tiles   */
+#define CG_OPT_DETERMINISTIC 4  /* split-K partials summed in a fixed order (run-to-run
+                                   bit-identical); default adds them in L2 (faster,
+                                   last-bit differences between runs)                  */
 
 typedef struct cg_layer cg_layer;
 
@@ -118,6 +121,17 @@ int cg_layer_query(const cg_layer* layer, cg_layer_info* info);
  *   y : (rows, n) float32, row-major
  */
 int cg_layer_gemm(cg_layer* layer, const void* x, int n, float* y, int mode, void* stream);
+
+/*
+ * Grouped launch: y_i = W_i x_i for `count` (1..8) independent layers in ONE
+ * launch of the fused kernel (e.g. the q/k/v or gate/up projections of a
+ * decoder block, which read the same x).  Layers must share v, m, the code
+ * width class (b <= 4 or b <= 8) and the device, and must all have
+ * fast_supported.  Device buffers, n columns each, stream-ordered.  Outputs
+ * are bit-identical to separate cg_layer_gemm calls (CG_MODE_FAST).
+ */
+int cg_gemm_group(cg_layer* const* layers, const void* const* xs, float* const* ys, int count,
+                  int n, void* stream);
 
 /* Same with HOST buffers: copies x in, runs, copies y out, synchronises. */
 int cg_layer_gemm_host(cg_layer* layer, const uint16_t* x, int n, float* y, int mode,

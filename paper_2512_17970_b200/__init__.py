@@ -15,6 +15,7 @@ from .engines import (
     build_psumbook,
     closed_form_counters,
     codegemm_gemm,
+    gemm_group,
     phase_split,
 )
 from .errors import (
@@ -48,6 +49,6 @@ __all__ = [
     "DeviceLayer", "DimOverflowError", "FormatError", "IntegrityError", "Matrix", "OpCounters",
     "Psumbook", "QuantConfig", "QuantizedLayer", "ScalePlane", "ShapeError", "TileConfig",
     "TruncatedFileError", "UnsupportedVersionError", "build_psumbook", "closed_form_counters",
-    "codegemm_gemm", "encode_f16_array", "pack_codes", "phase_split", "random_layer",
+    "codegemm_gemm", "encode_f16_array", "gemm_group", "pack_codes", "phase_split", "random_layer",
     "unpack_codes",
 ]

@@ -29,6 +29,7 @@ CG_MODE_STRICT = 2
 
 CG_OPT_NO_PDL = 1
 CG_OPT_NO_L2_PREFETCH = 2
+CG_OPT_DETERMINISTIC = 4
 
 MODES = {"auto": CG_MODE_AUTO, "fast": CG_MODE_FAST, "strict": CG_MODE_STRICT}
 
@@ -42,6 +43,7 @@ EXPORTS = (
     "cg_layer_query",
     "cg_layer_gemm",
     "cg_layer_gemm_host",
+    "cg_gemm_group",
     "cg_layer_psumbook",
     "cg_layer_unpack_codes",
     "cg_psumbook_build",
@@ -108,6 +110,9 @@ def load() -> ctypes.CDLL:
     lib.cg_layer_query.restype = i
     lib.cg_layer_gemm.argtypes = [vp, p, i, p, i, vp]
     lib.cg_layer_gemm.restype = i
+    lib.cg_gemm_group.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), i,
+                                  i, vp]
+    lib.cg_gemm_group.restype = i
     lib.cg_layer_gemm_host.argtypes = [vp, p, i, p, i, vp]
     lib.cg_layer_gemm_host.restype = i
     lib.cg_layer_psumbook.argtypes = [vp, p, i, p, vp]

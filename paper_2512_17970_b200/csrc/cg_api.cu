@@ -101,13 +101,15 @@ void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms, int reserved) {
             int64_t lo = 0, hi = 1 << 16;
             while (lo < hi) {  // largest rg count whose layout fits
                 const int64_t mid = (lo + hi + 1) / 2;
-                if (cg::smem_layout(z, (int)(mid * n_gs * 32), reserved, &lay)) lo = mid;
+                if (cg::smem_layout(z, (int)(mid * n_gs * 32), (int)(mid + 32) * 16, reserved,
+                                    &lay))
+                    lo = mid;
                 else hi = mid - 1;
             }
             rg_cap = lo;
         }
         if (rg_cap < 1) continue;
-        const int occ = 1;  // 512 threads x >100 registers: one CTA per SM
+        const int occ = 1;  // 512 threads x 128 registers: one CTA per SM
         int64_t rg_per_task;
         if (force_rg) {
             rg_per_task = force_rg;
@@ -124,11 +126,12 @@ void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms, int reserved) {
         const int64_t n_rb = (n_rg + rg_per_task - 1) / rg_per_task;
         const int64_t tasks = n_slices * n_rb;
         cg::SmemLayout lay;
-        cg::smem_layout(z, (int)(rg_per_task * n_gs * 32), reserved, &lay);
+        cg::smem_layout(z, (int)(rg_per_task * n_gs * 32), (int)(rg_per_task + 32) * 16, reserved,
+                        &lay);
         const double per_task = (double)rg_per_task * 16.0 * (u * p.m + 1) +
                                 (double)p.m * u * (1 << p.kbits) + 600.0;
         const double waves = std::ceil((double)tasks / ((double)sms * occ));
-        const double cost = waves * per_task * occ + (n_slices > 1 ? 16.0 * rg_per_task : 0.0);
+        const double cost = waves * per_task * occ;
         if (cost < best) {
             best = cost;
             p.fast = true;
@@ -162,8 +165,10 @@ struct cg_layer {
     uint16_t* scales = nullptr;     // (rows, groups) binary16
     uint16_t* books = nullptr;      // (m, 2**b, v) binary16
     float* ws = nullptr;            // split-K workspace (n_slices, rows, ws_cols)
-    unsigned long long* counters = nullptr;  // split-K tickets, one per row block (monotonic)
+    unsigned long long* tickets = nullptr;  // split-K tickets (n_rg, ws_cols), monotonic
+    unsigned long long* zero_ticket = nullptr;  // grid ticket of launches led by this layer
     int ws_cols = 0;
+    int reserved = 1024;            // driver-reserved smem at the start of the CTA window
     uint16_t* x_dev = nullptr;      // staging for the host entry point
     float* y_dev = nullptr;
     int stage_cols = 0;
@@ -198,7 +203,8 @@ void free_layer(cg_layer* L) {
     cudaFree(L->scales);
     cudaFree(L->books);
     cudaFree(L->ws);
-    cudaFree(L->counters);
+    cudaFree(L->tickets);
+    cudaFree(L->zero_ticket);
     cudaFree(L->stamps);
     cudaFree(L->x_dev);
     cudaFree(L->y_dev);
@@ -226,19 +232,131 @@ int ensure_ws(cg_layer* L, int n) {
     if (!p.fast || p.n_slices <= 1 || n <= L->ws_cols) return CG_OK;
     if (L->ws) {
         cudaFree(L->ws);
-        L->device_bytes -= (int64_t)p.n_slices * p.rows * L->ws_cols * 4;
+        cudaFree(L->tickets);
+        L->device_bytes -= (int64_t)p.n_slices * p.rows * L->ws_cols * 4 + p.n_rg * L->ws_cols * 8;
         L->ws = nullptr;
+        L->tickets = nullptr;
     }
     int rc = dev_alloc(L, &L->ws, (size_t)p.n_slices * p.rows * n * 4, "workspace alloc");
     if (rc) return rc;
-    // one monotonic ticket per row block; allocated and zeroed once
-    if (!L->counters) {
-        rc = dev_alloc(L, &L->counters, (size_t)p.n_rb * 8, "ticket alloc");
-        if (rc) return rc;
-        cudaError_t e = cudaMemset(L->counters, 0, (size_t)p.n_rb * 8);
-        if (e != cudaSuccess) return cuda_fail(e, "ticket init");
-    }
+    // one monotonic ticket per (row group, column): +n_slices per call
+    rc = dev_alloc(L, &L->tickets, (size_t)p.n_rg * n * 8, "ticket alloc");
+    if (rc) return rc;
+    cudaError_t e = cudaMemset(L->tickets, 0, (size_t)p.n_rg * n * 8);
+    if (e != cudaSuccess) return cuda_fail(e, "ticket init");
     L->ws_cols = n;
+    return CG_OK;
+}
+
+cg::LayerTask task_of(const cg_layer* L, const uint16_t* x, float* y) {
+    const cg::Plan& p = L->plan;
+    cg::LayerTask t{};
+    t.codes = L->codes;
+    t.scl = L->scl;
+    t.books = L->books;
+    t.x = x;
+    t.y = y;
+    t.ws = L->ws;
+    t.tickets = L->tickets;
+    t.rows = p.rows;
+    t.cols = p.cols;
+    t.n_rg = p.n_rg;
+    t.n_slices = p.n_slices;
+    t.n_rb = p.n_rb;
+    t.u = p.u;
+    t.rg_per_task = p.rg_per_task;
+    t.lg = p.lg;
+    t.n_gs = p.n_gs;
+    t.kcount = p.kcount;
+    t.n_tasks = (int)(p.n_slices * p.n_rb);
+    return t;
+}
+
+// One launch of the fused kernel for `count` layers (all fast, same v/m/u/kbits/device).
+int launch_same_u(cg_layer* const* layers, const uint16_t* const* xs, float* const* ys, int count,
+                 int n, cudaStream_t s) {
+    if (count < 1 || count > cg::kMaxGroup)
+        return fail(CG_ERR_ARG, "group size %d outside 1..%d", count, cg::kMaxGroup);
+    const cg::Plan& p0 = layers[0]->plan;
+    cg::GroupParams gp{};
+    gp.n_layers = count;
+    gp.n = n;
+    gp.flags = (layers[0]->flags & CG_OPT_NO_L2_PREFETCH) ? cg::kFlagNoPrefetch : 0;
+    gp.pf_dist = layers[0]->pf_dist;
+    gp.stamps = layers[0]->stamps;
+    cg::FusedSizes zmax{0, 0, 0};
+    int scl_max = 0, rg_max = 0, grid = 1;
+    for (int i = 0; i < count; ++i) {
+        cg_layer* L = layers[i];
+        const cg::Plan& p = L->plan;
+        if (!p.fast) return fail(CG_ERR_UNSUPPORTED, "layer %d has no fused kernel", i);
+        if (p.v != p0.v || p.m != p0.m || p.kbits != p0.kbits || p.u != p0.u ||
+            L->device != layers[0]->device)
+            return fail(CG_ERR_CONFIG, "group layers must share v, m, code width and device");
+        int rc = ensure_ws(L, n);
+        if (rc) return rc;
+        gp.layer[i] = task_of(L, xs[i], ys[i]);
+        cg::FusedSizes z;
+        cg::fused_sizes(p.v, p.m, p.u, p.kbits, &z);
+        zmax.psum = std::max(zmax.psum, z.psum);
+        zmax.books = std::max(zmax.books, z.books);
+        zmax.x = std::max(zmax.x, z.x);
+        scl_max = std::max(scl_max, p.rg_per_task * p.n_gs * 32);
+        rg_max = std::max(rg_max, p.rg_per_task);
+        grid = std::max(grid, gp.layer[i].n_tasks);
+    }
+    // persistent grid (one wave); if a layer has more tasks than CTAs, the CTA
+    // runs several tasks of it and split-K falls back to last-arriver sums
+    bool multi = grid > layers[0]->sms;
+    grid = std::min(grid, layers[0]->sms);
+    if (multi) gp.flags |= cg::kFlagLastArriver;
+    // fix-up list / owned-ticket targets (deterministic) or the staging buffer
+    // of a task's partial rows (reduce-add): the larger of the two
+    const int cap = rg_max * n + 16;
+    const int list_bytes = std::max(cap * 16, rg_max * 16 * n * 4);
+    cg::SmemLayout lay;
+    if (!cg::smem_layout(zmax, scl_max, list_bytes, layers[0]->reserved, &lay))
+        return fail(CG_ERR_CONFIG,
+                    "fused kernel does not fit in shared memory at n=%d (rows per task %d); "
+                    "use fewer columns per call or CG_MODE_STRICT", n, rg_max);
+    gp.off_psum = lay.off_psum;
+    gp.off_books = lay.off_books;
+    gp.off_x = lay.off_x;
+    gp.off_scl = lay.off_scl;
+    gp.off_bar = lay.off_bar;
+    gp.off_list = lay.off_list;
+    gp.off_stage = lay.off_list;
+    gp.list_cap = cap;
+    gp.zero_ticket = layers[0]->zero_ticket;
+    if (layers[0]->flags & CG_OPT_DETERMINISTIC) gp.flags |= cg::kFlagDeterministic;
+    const bool pdl = !(layers[0]->flags & CG_OPT_NO_PDL);
+    CG_CUDA(cg::launch_group_gemv(p0.v, p0.m, p0.u, p0.kbits, gp, grid, lay.total, pdl, s),
+            "fused gemv launch");
+    return CG_OK;
+}
+
+// Group launch: layers are partitioned by their tiling u (one kernel
+// instantiation per u); each partition is one launch, in first-seen order.
+int launch_group(cg_layer* const* layers, const uint16_t* const* xs, float* const* ys, int count,
+                 int n, cudaStream_t s) {
+    bool done[cg::kMaxGroup] = {false};
+    for (int i = 0; i < count; ++i) {
+        if (done[i]) continue;
+        cg_layer* part[cg::kMaxGroup];
+        const uint16_t* px[cg::kMaxGroup];
+        float* py[cg::kMaxGroup];
+        int k = 0;
+        for (int j = i; j < count; ++j) {
+            if (done[j] || layers[j]->plan.u != layers[i]->plan.u) continue;
+            part[k] = layers[j];
+            px[k] = xs[j];
+            py[k] = ys[j];
+            ++k;
+            done[j] = true;
+        }
+        int rc = launch_same_u(part, px, py, k, n, s);
+        if (rc) return rc;
+    }
     return CG_OK;
 }
 
@@ -255,41 +373,10 @@ int run_gemm(cg_layer* L, const uint16_t* x, int n, float* y, int mode, cudaStre
         return CG_OK;
     }
     if (mode != CG_MODE_FAST) return fail(CG_ERR_ARG, "unknown mode %d", mode);
-    int rc = ensure_ws(L, n);
-    if (rc) return rc;
-    const bool split = p.n_slices > 1;
-    const bool pdl = !(L->flags & CG_OPT_NO_PDL);
-    cg::GatherParams gp{};
-    gp.codes = L->codes;
-    gp.scl = L->scl;
-    gp.books = L->books;
-    gp.x = x;
-    gp.y = y;
-    gp.ws = L->ws;
-    gp.counters = L->counters;
-    gp.rows = p.rows;
-    gp.cols = p.cols;
-    gp.n_rg = p.n_rg;
-    gp.n_slices = p.n_slices;
-    gp.n_rb = p.n_rb;
-    gp.n = n;
-    gp.kcount = p.kcount;
-    gp.rg_per_task = p.rg_per_task;
-    gp.lg = p.lg;
-    gp.n_gs = p.n_gs;
-    gp.flags = (L->flags & CG_OPT_NO_L2_PREFETCH) ? cg::kFlagNoPrefetch : 0;
-    gp.pf_dist = L->pf_dist;
-    if (p.n_slices * p.n_rb > L->sms) gp.flags |= cg::kFlagLastArriver;
-    if (const char* e = std::getenv("CG_DEBUG_FLAGS")) gp.flags |= std::atoi(e);
-    gp.stamps = L->stamps;
-    gp.off_psum = p.smem.off_psum;
-    gp.off_books = p.smem.off_books;
-    gp.off_x = p.smem.off_x;
-    gp.off_scl = p.smem.off_scl;
-    gp.off_bar = p.smem.off_bar;
-    (void)split;  // split-K partials are summed inside the fused kernel (last-CTA fix-up)
-    CG_CUDA(cg::launch_fused_gemv(p, gp, pdl, s), "fused gemv launch");
-    return CG_OK;
+    cg_layer* one[1] = {L};
+    const uint16_t* xs[1] = {x};
+    float* ys[1] = {y};
+    return launch_group(one, xs, ys, 1, n, s);
 }
 
 }  // namespace
@@ -364,6 +451,7 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
     if (cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device) !=
         cudaSuccess)
         reserved = 1024;
+    L->reserved = reserved;
     plan_fast(p, opts ? opts->u : 0, opts ? opts->rg_per_task : 0, sm_count_of(device), reserved);
     if (opts && opts->u && !p.fast) {
         free_layer(L);
@@ -431,6 +519,10 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
     if (p.fast && p.n_slices > 1) {
         if ((rc = ensure_ws(L, 1))) return bail(rc);
     }
+    if (p.fast) {
+        if ((rc = dev_alloc(L, &L->zero_ticket, 16, "grid ticket"))) return bail(rc);
+        cudaMemset(L->zero_ticket, 0, 16);
+    }
     if (p.fast && std::getenv("CG_STAMPS")) {
         if ((rc = dev_alloc(L, &L->stamps, (size_t)p.n_slices * p.n_rb * 64, "stamps")))
             return bail(rc);
@@ -477,6 +569,19 @@ int cg_layer_gemm(cg_layer* L, const void* x, int n, float* y, int mode, void* s
                     static_cast<cudaStream_t>(stream));
 }
 
+int cg_gemm_group(cg_layer* const* layers, const void* const* xs, float* const* ys, int count,
+                  int n, void* stream) {
+    if (!layers || !xs || !ys) return fail(CG_ERR_ARG, "NULL layers/xs/ys");
+    if (count < 1 || count > cg::kMaxGroup)
+        return fail(CG_ERR_ARG, "group size %d outside 1..%d", count, cg::kMaxGroup);
+    if (n < 1) return fail(CG_ERR_SHAPE, "x must have >= 1 column, got %d", n);
+    for (int i = 0; i < count; ++i)
+        if (!layers[i] || !xs[i] || !ys[i]) return fail(CG_ERR_ARG, "NULL entry %d", i);
+    DeviceGuard guard(layers[0]->device);
+    return launch_group(layers, reinterpret_cast<const uint16_t* const*>(xs), ys, count, n,
+                        static_cast<cudaStream_t>(stream));
+}
+
 int cg_layer_gemm_host(cg_layer* L, const uint16_t* x, int n, float* y, int mode, void* stream) {
     if (!L || !x || !y) return fail(CG_ERR_ARG, "NULL layer/x/y");
     if (n < 1) return fail(CG_ERR_SHAPE, "x must have >= 1 column, got %d", n);
@@ -515,16 +620,16 @@ int cg_layer_psumbook(cg_layer* L, const void* x, int n, float* out, void* strea
     const cg::Plan& p = L->plan;
     if (!p.fast) return fail(CG_ERR_UNSUPPORTED, "layer has no fused kernel");
     DeviceGuard guard(L->device);
-    cg::GatherParams gp{};
-    gp.books = L->books;
-    gp.x = static_cast<const uint16_t*>(x);
-    gp.cols = p.cols;
-    gp.n = n;
-    gp.kcount = p.kcount;
-    gp.off_psum = p.smem.off_psum;
-    gp.off_books = p.smem.off_books;
-    gp.off_x = p.smem.off_x;
-    CG_CUDA(cg::launch_psumbook_dump(p, gp, out, static_cast<cudaStream_t>(stream)),
+    cg::DumpParams dp{};
+    dp.books = L->books;
+    dp.x = static_cast<const uint16_t*>(x);
+    dp.cols = p.cols;
+    dp.n = n;
+    dp.kcount = p.kcount;
+    dp.off_psum = p.smem.off_psum;
+    dp.off_books = p.smem.off_books;
+    dp.off_x = p.smem.off_x;
+    CG_CUDA(cg::launch_psumbook_dump(p, dp, out, static_cast<cudaStream_t>(stream)),
             "psumbook dump launch");
     return CG_OK;
 }

@@ -26,29 +26,49 @@ constexpr int kThreads = 512;  // fused kernel CTA size (16 warps)
 constexpr int kWarps = kThreads / 32;
 
 
-struct GatherParams {
+// One layer of a (group) launch of the fused kernel, passed by value.
+struct LayerTask {
     const uint8_t* codes;     // prepacked code tiles
     const uint16_t* scl;      // prepacked scale tiles (binary16 bits)
-    const uint16_t* books;    // (m, kcount_real, v) binary16 bits
+    const uint16_t* books;    // (m, kcount, v) binary16 bits
     const uint16_t* x;        // (cols, n) binary16 bits
     float* y;                 // (rows, n) output
     float* ws;                // split-K partials (n_slices, rows, n) when n_slices > 1
-    unsigned long long* counters;  // n_rb monotonic split-K tickets
+    unsigned long long* tickets;  // (n_rg, n) monotonic split-K tickets
     int64_t rows, cols, n_rg, n_slices, n_rb;
-    int n, kcount, rg_per_task, lg, n_gs, flags;
-    int pf_dist;              // row groups each warp prefetches ahead into L2 (0 = off)
-    unsigned long long* stamps;  // diagnostics: per-CTA phase timestamps (8 per CTA) or null
-    // dynamic shared-memory layout (bytes from the dynamic smem start); the
-    // Psumbook sits at a 64 KB-aligned shared-window address (see cg_api.cu)
-    int off_psum, off_books, off_x, off_scl, off_bar;
+    int u, rg_per_task, lg, n_gs, kcount, n_tasks;
 };
 
-// flags inside GatherParams
+constexpr int kMaxGroup = 8;
+
+// A launch: up to kMaxGroup independent layers sharing (v, m, u, table size)
+// and batch width n.  CTA c runs tasks c, c+grid, ... of every layer in order.
+struct GroupParams {
+    LayerTask layer[kMaxGroup];
+    int n_layers;
+    int n;                    // batch columns
+    int flags, pf_dist;
+    // dynamic shared-memory layout (bytes from the dynamic smem start); the
+    // Psumbook sits at a 64 KB-aligned shared-window address (see cg_api.cu)
+    int off_psum, off_books, off_x, off_scl, off_bar, off_list, list_cap;
+    int off_stage;            // split-K staging of a task's partial rows (atomic mode)
+    unsigned long long* zero_ticket;  // {count, generation}: every CTA zeroed its share of y
+    unsigned long long* stamps;  // diagnostics: per-CTA phase timestamps (8 per CTA) or null
+};
+
+// Psumbook dump (bit-exactness check of the fused kernel's on-chip table)
+struct DumpParams {
+    const uint16_t* books;
+    const uint16_t* x;
+    int64_t cols;
+    int n, kcount;
+    int off_psum, off_books, off_x;
+};
+
+// flags
 constexpr int kFlagNoPrefetch = 2;
-constexpr int kFlagLastArriver = 4;
-constexpr int kFlagNoCoop = 8;        // one wave without the cooperative launch attribute   // grid > one wave: last CTA of a row block sums it
-constexpr int kFlagDbgNoLookup = 64;  // diagnostics (CG_DEBUG_FLAGS): stream codes only
-constexpr int kFlagDbgNoLoad = 128;   // diagnostics: gather without streaming new codes
+constexpr int kFlagLastArriver = 4;  // a layer has more tasks than the grid: last arriver sums
+constexpr int kFlagDeterministic = 16;  // split-K by tickets + ordered sums (else L2 reduce-add)
 
 // shared-memory pieces of the fused kernel for (v, m, u, kbits)
 struct FusedSizes {
@@ -61,9 +81,12 @@ bool fused_sizes(int v, int m, int u, int kbits, FusedSizes* out);
 // the CTA's shared window so that one PRMT builds a whole lookup address; the
 // dynamic area starts `reserved` bytes into the window (1 KB on sm_100).
 struct SmemLayout {
-    int off_psum = 0, off_books = 0, off_x = 0, off_scl = 0, off_bar = 0, total = 0;
+    int off_psum = 0, off_books = 0, off_x = 0, off_scl = 0, off_bar = 0, off_list = 0, total = 0;
 };
-inline bool smem_layout(const FusedSizes& z, int scl_bytes, int reserved, SmemLayout* L) {
+// list_bytes covers the fix-up list (deterministic mode) or the split-K
+// staging buffer (reduce-add mode), whichever is larger
+inline bool smem_layout(const FusedSizes& z, int scl_bytes, int list_bytes, int reserved,
+                        SmemLayout* L) {
     auto up = [](int v, int a) { return (v + a - 1) / a * a; };
     const int kMax = 227 * 1024;
     int low = 0;
@@ -71,8 +94,10 @@ inline bool smem_layout(const FusedSizes& z, int scl_bytes, int reserved, SmemLa
     low = up(low + z.x, 16);
     L->off_scl = low;
     low = up(low + scl_bytes, 16);
+    L->off_list = low;
+    low = up(low + list_bytes, 16);
     L->off_bar = low;
-    low = up(low + 16, 16);
+    low = up(low + 64, 16);  // CtaState: mbarrier, fix-up count, previous task, grid gen
     const int gap = up(reserved + low, 65536) - reserved;  // first aligned slot
     if (gap - low >= z.books) {                           // books fit below
         L->off_books = low;
@@ -115,9 +140,10 @@ cudaError_t launch_prepack_scales(const Plan& p, const uint16_t* raw, uint16_t* 
 cudaError_t launch_check_codes(const Plan& p, const uint16_t* raw, unsigned* bad, cudaStream_t s);
 cudaError_t launch_unpack_codes(const Plan& p, const uint8_t* packed, const uint16_t* raw16,
                                 uint16_t* out, cudaStream_t s);
-cudaError_t launch_fused_gemv(const Plan& p, const GatherParams& gp, bool pdl, cudaStream_t s);
-cudaError_t launch_psumbook_dump(const Plan& p, const GatherParams& gp, float* out,
-                                 cudaStream_t s);
+// group launch: all layers share (v, m, kbits); grid = persistent CTAs
+cudaError_t launch_group_gemv(int v, int m, int u, int kbits, const GroupParams& gp, int grid,
+                              int smem, bool pdl, cudaStream_t s);
+cudaError_t launch_psumbook_dump(const Plan& p, const DumpParams& dp, float* out, cudaStream_t s);
 cudaError_t launch_strict_gemm(const Plan& p, const uint8_t* packed, const uint16_t* raw16,
                                const uint16_t* books, const uint16_t* scales, const uint16_t* x,
                                int n, float* y, cudaStream_t s);

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "cg_internal.h"
 
@@ -403,6 +404,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// split-K partials of a task: smem -> global y, added in L2 by the bulk engine
+__device__ __forceinline__ void bulk_reduce_add_f32(float* dst, const float* src, uint32_t bytes) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile(
+        "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+        "r"(smem_u32(src)), "r"(bytes)
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P;\n"
@@ -414,16 +431,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------------------
-// K2: fused Psumbook build + code-gather accumulate
+// K2: fused Psumbook build + code-gather accumulate (persistent, task-driven)
 //
-// One CTA = one task (K-slice, block of row groups).  Prologue: bulk-prefetch
-// the task's code stream to L2, bulk-copy its scale tiles to smem (TMA 1-D,
-// mbarrier), load codebooks and the first code tile to registers -- all of it
-// weights, so it overlaps the previous kernel under PDL -- then wait for the
-// producer of x, build the slice Psumbook.  Gather: each warp walks its row
-// groups with a two-deep register pipeline (ping-pong buffers, no copies).
-// Split-K: partials go to the workspace; the last CTA of a row block (atomic
-// ticket) sums the slices in ascending order -- deterministic, no 2nd kernel.
+// A launch runs a group of independent layers; CTA c executes tasks c,
+// c+grid, ... of each layer in order (a task = one K-slice x one block of row
+// groups).  Per task: the codebooks, the x slice and the first code tiles are
+// put in flight, the task's scale tiles arrive by bulk async copy (TMA 1-D,
+// mbarrier), the slice Psumbook is built in shared memory, and each warp walks
+// its row groups with a two-deep register pipeline.
+//
+// Split-K without barriers: a row group's partial goes to the workspace and
+// the writing warp takes a ticket on a monotonic per-row-group counter; the
+// slice that arrives last for a row group sums that row group over all
+// slices (fixed order -- deterministic).  The ticket is read one row group
+// later (its round trip overlaps the next lookups) and the sums run at the
+// start of the CTA's next task, overlapping that task's input loads.
 // ---------------------------------------------------------------------------
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ void load_tile(uint4 (&cw)[M][U], const uint8_t* tp) {
@@ -485,219 +507,338 @@ __device__ __forceinline__ float gather_row_group(const uint4 (&cw)[M][U], const
     return a[0];
 }
 
+// y[row][col] = sum over slices of the partials, slices ascending: the fixed
+// order that makes the split-K result independent of scheduling and tiling.
+__device__ __forceinline__ float sum_slices(const LayerTask& L, int n, int64_t row, int col) {
+    const int ns = (int)L.n_slices;
+    const int64_t plane = L.rows * n;
+    const float* src = L.ws + row * n + col;
+    float acc = 0.0f;
+    for (int s0 = 0; s0 < ns; s0 += 16) {
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (s0 + k < ns) v[k] = __ldcg(src + (int64_t)(s0 + k) * plane);
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (s0 + k < ns) acc = (s0 + k == 0) ? v[k] : acc + v[k];
+    }
+    return acc;
+}
+
+// whole row group (16 rows) by lanes 0-15 of a warp
+__device__ __noinline__ void fixup_row_group(const LayerTask& L, int n, int64_t rg, int col,
+                                             int lane) {
+    const int64_t row = rg * 16 + lane;
+    if (lane < 16 && row < L.rows) L.y[row * n + col] = sum_slices(L, n, row, col);
+}
+
+struct FixupEntry {
+    int layer, col;
+    long long rg;
+};
+
+// CTA-uniform state kept in shared memory (off_bar), not registers: the
+// mbarrier, the fix-up count, the previous task (closed at the start of the
+// next task, after that task's input loads are in flight, or at kernel end)
+// and the zero-barrier generation.
+struct CtaState {
+    uint64_t scl_bar;             // mbarrier of the scale-tile bulk copy
+    int list_count;
+    unsigned bar_phase;
+    unsigned long long zero_gen;  // grid generation seen at arrival
+    int zero_ready;
+    int prev_layer;
+    long long prev_slice, prev_rg0, prev_rg1;
+};
+struct PrevTask {
+    int layer;
+    long long slice, rg0, rg1;
+};
+
+// Split-K close of a task.  Every (row group, column) of the task takes a
+// ticket (acq_rel atomic: releases our partials, acquires the others').
+// Owner mode (persistent grid, one task per layer per CTA): slice s owns the
+// s-th 1/n_slices of the row block's row groups; it waits until all slices
+// have arrived on its row groups and sums them.  The wait is only on tasks of
+// earlier layers (or at kernel end), which never wait on us: no deadlock.
+// Last-arriver mode (grids beyond one wave): whoever arrives last sums.
+__device__ void close_task(const GroupParams& p, unsigned char* smem_raw, int tid) {
+    CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
+    const PrevTask prev{cs.prev_layer, cs.prev_slice, cs.prev_rg0, cs.prev_rg1};
+    if (prev.layer < 0) return;
+    const LayerTask& L = p.layer[prev.layer];
+    if (L.n_slices <= 1) return;
+    const int n = p.n, lane = tid & 31, warp = tid >> 5;
+    const unsigned long long ns = (unsigned long long)L.n_slices;
+    int* list_count = &cs.list_count;
+    const int64_t nrg = prev.rg1 - prev.rg0;
+    const bool owner_mode = !(p.flags & kFlagLastArriver);
+    const int64_t share = (nrg + (int64_t)ns - 1) / (int64_t)ns;
+    const int64_t own0 = prev.rg0 + prev.slice * share;
+    const int64_t own1 = min(own0 + share, (int64_t)prev.rg1);
+    unsigned long long* targets = reinterpret_cast<unsigned long long*>(smem_raw + p.off_list);
+    FixupEntry* list = reinterpret_cast<FixupEntry*>(smem_raw + p.off_list);
+    for (int64_t e = tid; e < nrg * n; e += kThreads) {
+        const int64_t rg = prev.rg0 + e / n;
+        const int col = (int)(e % n);
+        unsigned long long old;
+        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
+                     : "=l"(old)
+                     : "l"(L.tickets + rg * n + col)
+                     : "memory");
+        if (owner_mode) {
+            if (rg >= own0 && rg < own1) targets[(rg - own0) * n + col] = (old / ns + 1) * ns;
+        } else if (old % ns == ns - 1) {
+            const int slot = atomicAdd(list_count, 1);
+            list[slot] = FixupEntry{prev.layer, col, (long long)rg};
+        }
+    }
+    __syncthreads();
+    if (owner_mode) {
+        const int64_t nown = own1 > own0 ? own1 - own0 : 0;
+        // wait for the other slices on the owned row groups
+        for (int64_t e = tid; e < nown * n; e += kThreads) {
+            const unsigned long long* t = L.tickets + (own0 + e / n) * n + (e % n);
+            const unsigned long long want = targets[e];
+            unsigned long long cur;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(t) : "memory");
+            } while (cur < want);
+        }
+        __syncthreads();
+        // one thread per (row, column) of the owned row groups
+        const int64_t r_lo = own0 * 16, r_hi = min(own1 * 16, L.rows);
+        const int64_t nrows = r_hi > r_lo ? r_hi - r_lo : 0;
+        for (int64_t e = tid; e < nrows * n; e += kThreads) {
+            const int64_t row = r_lo + e / n;
+            const int col = (int)(e % n);
+            L.y[row * n + col] = sum_slices(L, n, row, col);
+        }
+    } else {
+        const int cnt = *list_count;
+        for (int e = warp; e < cnt; e += kWarps) {
+            const FixupEntry f = list[e];
+            fixup_row_group(p.layer[f.layer], n, f.rg, f.col, lane);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) *list_count = 0;
+}
+
+// reduce-add mode: the first split-K flush of a CTA waits until every CTA
+// has zeroed its share of the outputs (grid ticket taken at kernel start)
 template <int V, int M, int U, int KB>
-__global__ void __launch_bounds__(kThreads, 1) fused_gemv_kernel(const GatherParams p) {
+__device__ __forceinline__ void run_task(const GroupParams& p, int l, int64_t task, bool first_task,
+                                         unsigned char* smem_raw, int tid) {
     using S = FusedShape<V, M, U, KB>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const LayerTask& L = p.layer[l];
     float* psum = reinterpret_cast<float*>(smem_raw + p.off_psum);
     float2* books2 = reinterpret_cast<float2*>(smem_raw + p.off_books);
     float* x32 = reinterpret_cast<float*>(smem_raw + p.off_x);
     uint16_t* scl_s = reinterpret_cast<uint16_t*>(smem_raw + p.off_scl);
-    uint64_t& scl_bar = *reinterpret_cast<uint64_t*>(smem_raw + p.off_bar);
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t task = blockIdx.x;
-    const int64_t slice = task / p.n_rb;
-    const int64_t rb = task - slice * p.n_rb;
-    const int n = p.n;
-    const int64_t rg0 = rb * p.rg_per_task;
-    const int64_t rg1 = min(rg0 + (int64_t)p.rg_per_task, p.n_rg);
-    const int n_gs = p.n_gs;
-    const uint8_t* tiles = p.codes + slice * p.n_rg * (int64_t)S::kTileBytes;
-
-    unsigned long long* stamps = p.stamps ? p.stamps + blockIdx.x * 8 : nullptr;
+    CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
+    uint64_t* scl_bar = &cs.scl_bar;
+    unsigned long long* stamps =
+        (p.stamps && first_task && l == 0) ? p.stamps + blockIdx.x * 8 : nullptr;
 #define CG_STAMP(k) \
     if (stamps && tid == 0) stamps[k] = gtimer();
+
+    const int lane = tid & 31, warp = tid >> 5;
+    const int n = p.n;
+    const int64_t slice = task / L.n_rb;
+    const int64_t rb = task - slice * L.n_rb;
+    const int64_t rg0 = rb * L.rg_per_task;
+    const int64_t rg1 = min(rg0 + (int64_t)L.rg_per_task, L.n_rg);
+    const int n_gs = L.n_gs;
+    const uint8_t* tiles = L.codes + slice * L.n_rg * (int64_t)S::kTileBytes;
+    const bool split = L.n_slices > 1;
     CG_STAMP(0)
-    // 1. weights (independent of the previous kernel in the stream)
-    if (tid == 0) {
-        const uint32_t bytes = (uint32_t)((rg1 - rg0) * n_gs * 32);
-        mbar_init(&scl_bar, 1);
-        mbar_expect_tx(&scl_bar, bytes);
-        bulk_g2s(scl_s, p.scl + (slice * p.n_rg + rg0) * n_gs * 16, bytes, &scl_bar);
-    }
-    // progressive L2 prefetch: each warp keeps its next `pf` row groups in
-    // flight towards L2 (the bytes in flight, not the issue rate, bound HBM)
-    const int pf = (p.flags & kFlagNoPrefetch) ? 0 : p.pf_dist;
-    uint16_t breg[S::kBookPerThread];
-    load_books<V, M, U, KB>(breg, p.books, p.kcount, tid);
+
+    // 1. inputs of this task in flight: codebooks, x (column 0), first tiles -> L2
     const int my_rgs = rg0 + warp < rg1 ? (int)((rg1 - rg0 - warp + kWarps - 1) / kWarps) : 0;
     const uint8_t* cptr = tiles + (rg0 + warp) * S::kTileBytes + lane * 16;
     constexpr int64_t kStep = (int64_t)kWarps * S::kTileBytes;
-    const uint8_t* wtile = tiles + (rg0 + warp) * S::kTileBytes;  // this warp's tile 0
-    // the first two tiles go to L2 now; registers take them after the build
-    if (lane < 2 && lane < my_rgs) prefetch_l2_bulk(wtile + lane * kStep, S::kTileBytes);
-    if (lane >= 2 && lane < 2 + pf && lane < my_rgs)
-        prefetch_l2_bulk(wtile + lane * kStep, S::kTileBytes);
-    uint4 bufA[M][U], bufB[M][U];
+    const uint8_t* wtile = tiles + (rg0 + warp) * S::kTileBytes;
+    const int pf = (p.flags & kFlagNoPrefetch) ? 0 : p.pf_dist;
+    if (lane < 2 + pf && lane < my_rgs) prefetch_l2_bulk(wtile + lane * kStep, S::kTileBytes);
+    uint16_t breg[S::kBookPerThread];
+    load_books<V, M, U, KB>(breg, L.books, L.kcount, tid);
+    uint16_t xreg[S::kXPerThread];
+    load_x<V, M, U, KB>(xreg, L.x, slice, L.cols, n, 0, tid);
+
+    // 2. the previous task is done with tables, scales and the staging buffer;
+    //    close its row groups
+    if (tid == 0) bulk_wait_read();
+    __syncthreads();
+    if (tid == 0) {
+        const uint32_t bytes = (uint32_t)((rg1 - rg0) * n_gs * 32);
+        mbar_expect_tx(scl_bar, bytes);
+        bulk_g2s(scl_s, L.scl + (slice * L.n_rg + rg0) * n_gs * 16, bytes, scl_bar);
+    }
+    close_task(p, smem_raw, tid);
+    store_books<V, M, U, KB>(books2, breg, L.kcount, tid);
+    CG_STAMP(1)
 
     // per-lane constants of the gather (Psumbook base must be 64 KB aligned)
     const uint32_t psum_addr = smem_u32(psum);
     if (psum_addr & 0xffffu) __trap();
     const uint32_t lb0 = ((uint32_t)lane << 2) | ((psum_addr >> 16) << 8);
     const uint32_t lb1 = lb0 | 0x80u;
-    const int lg = p.lg;
+    const int lg = L.lg;
     const int ls = lg < 4 ? lg : 4;
     const int mask = row_mask(lane);
     const int sbase = mask & ~((16 >> ls) - 1);  // first row of this lane's scale run
     const int gi = lg >= 5 ? 0 : (lane >> lg);
-    const bool split = p.n_slices > 1;
     const uint16_t* sp0 = scl_s + (warp * n_gs + gi) * 16 + sbase;
     const int sstep = kWarps * n_gs * 16;
-    const int64_t row_step = (int64_t)kWarps * 16;
+    uint4 bufA[M][U], bufB[M][U];
 
-    // 2. per batch column: wait for x (PDL), build the slice Psumbook, gather
     for (int col = 0; col < n; ++col) {
-        if (col == 0) {
-            pdl_wait();
-        } else {
+        if (col > 0) {
             __syncthreads();  // previous column's table is no longer read
+            load_x<V, M, U, KB>(xreg, L.x, slice, L.cols, n, col, tid);
         }
-        uint16_t xreg[S::kXPerThread];
-        load_x<V, M, U, KB>(xreg, p.x, slice, p.cols, n, col, tid);
-        if (col == 0) store_books<V, M, U, KB>(books2, breg, p.kcount, tid);
         store_x<V, M, U, KB>(x32, xreg, tid);
         __syncthreads();
-        if (col == 0) CG_STAMP(1)
-        build_psumbook_smem<V, M, U, KB>(psum, books2, x32, p.kcount, tid);
+        build_psumbook_smem<V, M, U, KB>(psum, books2, x32, L.kcount, tid);
         __syncthreads();
-        if (p.flags & 512) return;  // diagnostics: prologue + build only
         if (my_rgs > 0) load_tile<V, M, U, KB>(bufA, cptr);
         if (col == 0) {
             CG_STAMP(2)
-            pdl_launch_dependents();
-            mbar_wait(&scl_bar, 0);
+            if (first_task) pdl_launch_dependents();
+            mbar_wait(scl_bar, cs.bar_phase);
         }
-        float* out = split ? p.ws + slice * p.rows * n : p.y;
+        const bool stage_out = split && !(p.flags & kFlagDeterministic);
+        float* out = stage_out ? reinterpret_cast<float*>(smem_raw + p.off_stage) - rg0 * 16 * n
+                               : (split ? L.ws + slice * L.rows * n : L.y);
         int64_t row = (rg0 + warp) * 16 + mask;
-        if (p.flags & kFlagDbgNoLookup) {  // diagnostic: stream the codes only
-            uint32_t acc = 0;
-            for (int i = 0; i < my_rgs; ++i) {
-                load_tile<V, M, U, KB>(bufA, cptr + i * kStep);
-#pragma unroll
-                for (int t = 0; t < M; ++t)
-#pragma unroll
-                    for (int c = 0; c < U; ++c)
-                        acc ^= bufA[t][c].x ^ bufA[t][c].y ^ bufA[t][c].z ^ bufA[t][c].w;
-            }
-            if (acc == 0x12345678u) out[0] = 1.0f;
-            continue;
-        }
-        const int64_t lstep = (p.flags & kFlagDbgNoLoad) ? 0 : kStep;
+        const int64_t row_step = (int64_t)kWarps * 16;
         for (int i = 0; i < my_rgs; i += 2) {
             if (col == 0 && lane < 2 && i + 1 + pf + lane < my_rgs && pf > 0)
                 prefetch_l2_bulk(wtile + (i + 1 + pf + lane) * kStep, S::kTileBytes);
-            if (i + 1 < my_rgs) load_tile<V, M, U, KB>(bufB, cptr + (i + 1) * lstep);
-            float v = gather_row_group<V, M, U, KB>(bufA, sp0 + i * sstep, lb0, lb1,
-                                                    lg, mask);
-            if (lane < 16 && row < p.rows) out[row * n + col] = v;
+            if (i + 1 < my_rgs) load_tile<V, M, U, KB>(bufB, cptr + (i + 1) * kStep);
+            float v = gather_row_group<V, M, U, KB>(bufA, sp0 + i * sstep, lb0, lb1, lg, mask);
+            if (lane < 16 && row < L.rows) out[row * n + col] = v;
             row += row_step;
             if (i + 1 < my_rgs) {
-                if (i + 2 < my_rgs) load_tile<V, M, U, KB>(bufA, cptr + (i + 2) * lstep);
-                v = gather_row_group<V, M, U, KB>(bufB, sp0 + (i + 1) * sstep, lb0, lb1,
-                                                  lg, mask);
-                if (lane < 16 && row < p.rows) out[row * n + col] = v;
+                if (i + 2 < my_rgs) load_tile<V, M, U, KB>(bufA, cptr + (i + 2) * kStep);
+                v = gather_row_group<V, M, U, KB>(bufB, sp0 + (i + 1) * sstep, lb0, lb1, lg, mask);
+                if (lane < 16 && row < L.rows) out[row * n + col] = v;
                 row += row_step;
             }
         }
     }
+    if (split && !(p.flags & kFlagDeterministic)) {
+        // flush the task's partial rows into y (L2 reduce-add); y was zeroed
+        // by the grid at kernel start -- wait for that once
+        __syncthreads();
+        if (tid == 0) {
+            if (!cs.zero_ready) {
+                // sense-reversal grid barrier on {count, generation}: wait for
+                // the generation recorded at arrival to move on
+                const unsigned long long g0 = cs.zero_gen;
+                unsigned long long cur;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];"
+                                 : "=l"(cur)
+                                 : "l"(p.zero_ticket + 1)
+                                 : "memory");
+                } while (cur == g0);
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                cs.zero_ready = 1;
+            }
+            const float* stage = reinterpret_cast<const float*>(smem_raw + p.off_stage);
+            const int64_t r1 = min(rg1 * 16, L.rows);
+            const int64_t elems = (r1 - rg0 * 16) * n;
+            const int64_t body = elems & ~int64_t(3);  // 16-byte multiple
+            if (body > 0) bulk_reduce_add_f32(L.y + rg0 * 16 * n, stage, (uint32_t)(body * 4));
+            for (int64_t e = body; e < elems; ++e) atomicAdd(L.y + rg0 * 16 * n + e, stage[e]);
+        }
+    }
     __syncthreads();
-    CG_STAMP(3)
-    if (!split) return;
-
-    // 3. split-K fix-up, shared by the n_slices CTAs of this row block: a
-    //    ticket barrier on a monotonic 64-bit counter (target = next multiple
-    //    of n_slices above our ticket; no reset, one atomic round trip; all
-    //    CTAs are co-resident: cooperative launch, one wave), then CTA `slice`
-    //    sums its 1/n_slices share of the rows over all slices in ascending
-    //    order -- deterministic.
-    int* s_flag = reinterpret_cast<int*>(smem_raw + p.off_bar + 8);
-    const bool one_wave = !(p.flags & kFlagLastArriver);
     if (tid == 0) {
-        unsigned long long* cnt = p.counters + rb;
-        __threadfence();
-        const unsigned long long ns = (unsigned long long)p.n_slices;
-        const unsigned long long old = atomicAdd(cnt, 1ull);
-        if (one_wave) {
-            const unsigned long long target = (old / ns + 1) * ns;
-            unsigned long long cur;
-            do {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(cnt) : "memory");
-            } while (cur < target);
-        } else {
-            *s_flag = (old % ns == ns - 1);  // last arriver of this row block
-            __threadfence();
-        }
+        cs.bar_phase ^= 1u;
+        cs.prev_layer = (split && (p.flags & kFlagDeterministic)) ? l : -1;
+        cs.prev_slice = slice;
+        cs.prev_rg0 = rg0;
+        cs.prev_rg1 = rg1;
     }
-    __syncthreads();
-    CG_STAMP(4)
-    if (!one_wave && !*s_flag) return;
-    const int64_t rows0 = rg0 * 16, rows1 = min(rg1 * 16, p.rows);
-    // one wave: CTA `slice` sums its share of the rows; otherwise the last
-    // arriver sums the whole row block
-    const int64_t share = one_wave
-        ? ((rows1 - rows0 + p.n_slices - 1) / p.n_slices + 3) & ~int64_t(3)
-        : rows1 - rows0;
-    const int64_t first = one_wave ? rows0 + slice * share : rows0;
-    const int64_t e_lo = first * n;
-    const int64_t e_hi = min(first + share, rows1) * n;
-    const int64_t plane = p.rows * n;
-    const int ns = (int)p.n_slices;
-    if ((plane & 3) == 0) {  // float4 over 4 consecutive outputs, 16 slices per round trip
-        for (int64_t e = e_lo + 4 * tid; e < e_hi; e += 4 * kThreads) {
-            const float* src = p.ws + e;
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int s0 = 0; s0 < ns; s0 += 16) {
-                float4 v[16];
-#pragma unroll
-                for (int s = 0; s < 16; ++s)
-                    if (s0 + s < ns)
-                        v[s] = __ldcg(reinterpret_cast<const float4*>(src + (int64_t)(s0 + s) * plane));
-#pragma unroll
-                for (int s = 0; s < 16; ++s)
-                    if (s0 + s < ns) {
-                        if (s0 + s == 0) {
-                            acc = v[s];
-                        } else {
-                            acc.x += v[s].x;
-                            acc.y += v[s].y;
-                            acc.z += v[s].z;
-                            acc.w += v[s].w;
-                        }
-                    }
-            }
-            if (e + 3 < e_hi) {
-                *reinterpret_cast<float4*>(p.y + e) = acc;
-            } else {
-                const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
-                for (int k = 0; k < 4 && e + k < e_hi; ++k) p.y[e + k] = a4[k];
-            }
-        }
-    } else {
-        for (int64_t e = e_lo + tid; e < e_hi; e += kThreads) {
-            const float* src = p.ws + e;
-            float acc = 0.0f;
-            for (int s0 = 0; s0 < ns; s0 += 16) {
-                float v[16];
-#pragma unroll
-                for (int s = 0; s < 16; ++s)
-                    if (s0 + s < ns) v[s] = __ldcg(src + (int64_t)(s0 + s) * plane);
-#pragma unroll
-                for (int s = 0; s < 16; ++s)
-                    if (s0 + s < ns) acc = (s0 + s == 0) ? v[s] : acc + v[s];
-            }
-            p.y[e] = acc;
-        }
-    }
-    __syncthreads();
-    CG_STAMP(5)
+    CG_STAMP(3)
 #undef CG_STAMP
+}
+
+template <int V, int M, int U, int KB>
+__global__ void __launch_bounds__(kThreads, 1)
+    group_gemv_kernel(const __grid_constant__ GroupParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x;
+    CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
+    if (tid == 0) {
+        mbar_init(&cs.scl_bar, 1);
+        cs.list_count = 0;
+        cs.bar_phase = 0;
+        cs.zero_ready = 0;
+        cs.prev_layer = -1;
+    }
+    bool first = true;
+    // every layer's x (and y, for write-after-read) belongs to earlier work
+    pdl_wait();
+    if (!(p.flags & kFlagDeterministic)) {
+        // zero this CTA's share of every split layer's output, then take the
+        // grid ticket (its round trip overlaps the first task)
+        bool any = false;
+        for (int l = 0; l < p.n_layers; ++l) {
+            const LayerTask& L = p.layer[l];
+            if (L.n_slices <= 1) continue;
+            any = true;
+            const int64_t elems = L.rows * p.n;
+            const int64_t per = (elems + gridDim.x - 1) / gridDim.x;
+            const int64_t e0 = blockIdx.x * per, e1 = min(e0 + per, elems);
+            for (int64_t e = e0 + tid; e < e1; e += kThreads) L.y[e] = 0.0f;
+        }
+        if (any) {
+            __syncthreads();
+            if (tid == 32) {  // arrive (tid 0 is busy issuing the first task's copies)
+                unsigned long long g, old;
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];"
+                             : "=l"(g)
+                             : "l"(p.zero_ticket + 1)
+                             : "memory");
+                cs.zero_gen = g;
+                asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
+                             : "=l"(old)
+                             : "l"(p.zero_ticket)
+                             : "memory");
+                if (old == (unsigned long long)gridDim.x - 1) {
+                    *reinterpret_cast<volatile unsigned long long*>(p.zero_ticket) = 0ull;
+                    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(p.zero_ticket + 1)
+                                 : "memory");
+                }
+            }
+        }
+    }
+    // (all layers of a launch share U: the host splits groups by u)
+    for (int l = 0; l < p.n_layers; ++l) {
+        for (int64_t t = blockIdx.x; t < p.layer[l].n_tasks; t += gridDim.x) {
+            run_task<V, M, U, KB>(p, l, t, first, smem_raw, tid);
+            first = false;
+        }
+    }
+    // close the last task's row groups; drain the bulk reduce-adds
+    __syncthreads();
+    close_task(p, smem_raw, tid);
+    if (tid == 0) bulk_wait_all();
+    if (p.stamps && tid == 0 && blockIdx.x < p.layer[0].n_tasks) {
+        __syncthreads();
+        p.stamps[blockIdx.x * 8 + 4] = gtimer();
+    }
 }
 
 // dump the fused kernel's smem Psumbook in _psum_tables layout (m, segs, 2**b, n)
 template <int V, int M, int U, int KB>
 __global__ void __launch_bounds__(kThreads, 1)
-    psumbook_dump_kernel(const GatherParams p, float* __restrict__ out, int64_t segs) {
+    psumbook_dump_kernel(const DumpParams p, float* __restrict__ out, int64_t segs) {
     using S = FusedShape<V, M, U, KB>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* psum = reinterpret_cast<float*>(smem_raw + p.off_psum);
@@ -791,20 +932,20 @@ int grid_for(int64_t total, int threads) {
 // template dispatch
 // ---------------------------------------------------------------------------
 template <int V, int M, int U, int KB>
-cudaError_t launch_fused_t(const GatherParams& gp, int64_t grid_x, int smem, bool pdl,
-                           cudaStream_t s) {
-    auto kern = fused_gemv_kernel<V, M, U, KB>;
+cudaError_t launch_group_t(const GroupParams& gp, int grid, int smem, bool pdl, cudaStream_t s) {
+    auto kern = group_gemv_kernel<V, M, U, KB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid_x, 1, 1);
+    cfg.gridDim = dim3((unsigned)grid, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    // cooperative: the split-K ticket barrier needs every CTA resident (one wave)
+    // owner-mode split-K waits on other CTAs: co-residency guaranteed by a
+    // cooperative launch of a persistent (<= one wave) grid
     cudaLaunchAttribute attr[2];
     int na = 0;
-    if (gp.n_slices > 1 && !(gp.flags & (kFlagLastArriver | kFlagNoCoop))) {
+    if (!(gp.flags & kFlagLastArriver)) {
         attr[na].id = cudaLaunchAttributeCooperative;
         attr[na].val.cooperative = 1;
         ++na;
@@ -820,41 +961,61 @@ cudaError_t launch_fused_t(const GatherParams& gp, int64_t grid_x, int smem, boo
 }
 
 template <int V, int M, int U, int KB>
-cudaError_t launch_dump_t(const GatherParams& gp, int64_t n_slices, float* out, int64_t segs,
+cudaError_t launch_dump_t(const DumpParams& dp, int64_t n_slices, float* out, int64_t segs,
                           int smem, cudaStream_t s) {
     auto kern = psumbook_dump_kernel<V, M, U, KB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    kern<<<dim3((unsigned)n_slices, (unsigned)gp.n), kThreads, smem, s>>>(gp, out, segs);
+    kern<<<dim3((unsigned)n_slices, (unsigned)dp.n), kThreads, smem, s>>>(dp, out, segs);
     return cudaGetLastError();
 }
 
-// Visit the instantiation for runtime (v, m, u, kb).  Instantiated set:
-// v in {2,4,8,16}, (m,u) in {(1,1),(1,2),(1,4),(2,1),(2,2),(3,1),(4,1)}, kb in {4,8}.
+// Instantiated set: v in {2,4,8,16}, m in {1,2,3,4}, kb in {4,8}; the group
+// kernel switches on u at run time among u in {1,2,4} with m*u <= 4.
 template <typename F>
-bool visit(int v, int m, int u, int kb, F&& f) {
-#define CG_KB(V_, M_, U_)                         \
-    if (kb == 4) return f.template run<V_, M_, U_, 4>(), true; \
-    if (kb == 8) return f.template run<V_, M_, U_, 8>(), true; \
+bool visit_vmk(int v, int m, int kb, F&& f) {
+#define CG_KB(V_, M_)                                  \
+    if (kb == 4) return f.template run<V_, M_, 4>(), true; \
+    if (kb == 8) return f.template run<V_, M_, 8>(), true; \
     return false;
-#define CG_MU(V_)                                  \
-    if (m == 1 && u == 1) { CG_KB(V_, 1, 1) }      \
-    if (m == 1 && u == 2) { CG_KB(V_, 1, 2) }      \
-    if (m == 1 && u == 4) { CG_KB(V_, 1, 4) }      \
-    if (m == 2 && u == 1) { CG_KB(V_, 2, 1) }      \
-    if (m == 2 && u == 2) { CG_KB(V_, 2, 2) }      \
-    if (m == 3 && u == 1) { CG_KB(V_, 3, 1) }      \
-    if (m == 4 && u == 1) { CG_KB(V_, 4, 1) }      \
+#define CG_M(V_)                      \
+    if (m == 1) { CG_KB(V_, 1) }      \
+    if (m == 2) { CG_KB(V_, 2) }      \
+    if (m == 3) { CG_KB(V_, 3) }      \
+    if (m == 4) { CG_KB(V_, 4) }      \
     return false;
     switch (v) {
-        case 2: { CG_MU(2) }
-        case 4: { CG_MU(4) }
-        case 8: { CG_MU(8) }
-        case 16: { CG_MU(16) }
+        case 2: { CG_M(2) }
+        case 4: { CG_M(4) }
+        case 8: { CG_M(8) }
+        case 16: { CG_M(16) }
         default: return false;
     }
-#undef CG_MU
+#undef CG_M
 #undef CG_KB
+}
+
+template <typename F>
+struct WithU {
+    F& f;
+    int u;
+    template <int V, int M, int KB>
+    void run() {
+        if constexpr (M * 4 <= 4) {
+            if (u == 4) { f.template run<V, M, 4, KB>(); return; }
+        }
+        if constexpr (M * 2 <= 4) {
+            if (u == 2) { f.template run<V, M, 2, KB>(); return; }
+        }
+        f.template run<V, M, 1, KB>();
+    }
+};
+
+template <typename F>
+bool visit(int v, int m, int u, int kb, F&& f) {
+    if (!(u == 1 || u == 2 || u == 4) || m * u > 4) return false;
+    WithU<std::remove_reference_t<F>> inner{f, u};
+    return visit_vmk(v, m, kb, inner);
 }
 
 struct SizeQuery {
@@ -865,18 +1026,17 @@ struct SizeQuery {
         z = FusedSizes{S::kPsumBytes, S::kBookBytes, S::kXBytes};
     }
 };
-struct FusedLaunch {
-    const GatherParams* gp;
-    int64_t grid_x;
-    int smem;
+struct GroupLaunch {
+    const GroupParams* gp;
+    int grid, smem;
     bool pdl;
     cudaStream_t s;
     cudaError_t err = cudaErrorInvalidConfiguration;
     template <int V, int M, int U, int KB>
-    void run() { err = launch_fused_t<V, M, U, KB>(*gp, grid_x, smem, pdl, s); }
+    void run() { err = launch_group_t<V, M, U, KB>(*gp, grid, smem, pdl, s); }
 };
 struct DumpLaunch {
-    const GatherParams* gp;
+    const DumpParams* dp;
     int64_t n_slices;
     float* out;
     int64_t segs;
@@ -884,7 +1044,7 @@ struct DumpLaunch {
     cudaStream_t s;
     cudaError_t err = cudaErrorInvalidConfiguration;
     template <int V, int M, int U, int KB>
-    void run() { err = launch_dump_t<V, M, U, KB>(*gp, n_slices, out, segs, smem, s); }
+    void run() { err = launch_dump_t<V, M, U, KB>(*dp, n_slices, out, segs, smem, s); }
 };
 
 }  // namespace
@@ -932,15 +1092,15 @@ cudaError_t launch_unpack_codes(const Plan& p, const uint8_t* packed, const uint
     return cudaGetLastError();
 }
 
-cudaError_t launch_fused_gemv(const Plan& p, const GatherParams& gp, bool pdl, cudaStream_t s) {
-    FusedLaunch f{&gp, p.n_slices * p.n_rb, p.smem.total, pdl, s};
-    if (!visit(p.v, p.m, p.u, p.kbits, f)) return cudaErrorInvalidConfiguration;
+cudaError_t launch_group_gemv(int v, int m, int u, int kbits, const GroupParams& gp, int grid,
+                              int smem, bool pdl, cudaStream_t s) {
+    GroupLaunch f{&gp, grid, smem, pdl, s};
+    if (!visit(v, m, u, kbits, f)) return cudaErrorInvalidConfiguration;
     return f.err;
 }
 
-cudaError_t launch_psumbook_dump(const Plan& p, const GatherParams& gp, float* out,
-                                 cudaStream_t s) {
-    DumpLaunch f{&gp, p.n_slices, out, p.segs, p.smem.total, s};
+cudaError_t launch_psumbook_dump(const Plan& p, const DumpParams& dp, float* out, cudaStream_t s) {
+    DumpLaunch f{&dp, p.n_slices, out, p.segs, p.smem.total, s};
     if (!visit(p.v, p.m, p.u, p.kbits, f)) return cudaErrorInvalidConfiguration;
     return f.err;
 }

@@ -224,6 +224,35 @@ class DeviceLayer:
         return out.cpu().numpy().view(np.uint16)
 
 
+def gemm_group(layers, xs, ys=None, stream=None):
+    """One fused launch (per tiling class) for several independent layers.
+
+    ``layers``: DeviceLayer objects sharing v, m and code width; ``xs``: CUDA
+    float16 (cols_i, n) tensors with the same n; returns the (rows_i, n)
+    float32 outputs, bit-identical to calling ``gemm`` on each layer.
+    """
+    import torch
+
+    if not layers or len(layers) != len(xs):
+        raise ShapeError("need one x per layer")
+    n = int(xs[0].shape[1])
+    xs = [x.contiguous() for x in xs]
+    for dl, x in zip(layers, xs):
+        if x.dtype != torch.float16 or x.dim() != 2 or x.shape[0] != dl.cols or x.shape[1] != n:
+            raise ShapeError(f"x for a {dl.rows}x{dl.cols} layer must be ({dl.cols}, {n}) float16")
+    if ys is None:
+        ys = [torch.empty((dl.rows, n), dtype=torch.float32, device=x.device)
+              for dl, x in zip(layers, xs)]
+    s = stream if stream is not None else torch.cuda.current_stream(xs[0].device)
+    lib = _lib.load()
+    k = len(layers)
+    hs = (ctypes.c_void_p * k)(*[dl.handle.value for dl in layers])
+    xp = (ctypes.c_void_p * k)(*[x.data_ptr() for x in xs])
+    yp = (ctypes.c_void_p * k)(*[y.data_ptr() for y in ys])
+    _lib.check(lib.cg_gemm_group(hs, xp, yp, k, n, ctypes.c_void_p(s.cuda_stream)))
+    return ys
+
+
 # one device copy per live layer object (weights are immutable)
 _CACHE: dict = {}
 

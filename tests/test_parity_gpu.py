@@ -11,6 +11,7 @@ import numpy as np
 import pytest
 
 import paper_2512_17970_b200 as cg
+from paper_2512_17970_b200 import _lib
 from helpers import assert_within_tolerance, layer_from_case, tolerance_report
 from oracle import c_oracle
 from oracle import codegemm_oracle as orc
@@ -183,24 +184,31 @@ def test_full_size_70b_shapes_vs_c_oracle(shape):
 # ---------------------------------------------------------------- invariances
 
 
+DET = _lib.CG_OPT_DETERMINISTIC
+
+
 def test_fast_mode_deterministic_and_tiling_invariant_per_u():
+    # deterministic split-K: bits independent of run, rows per task, grid waves
     q = cg.random_layer(1000, 4096, cg.QuantConfig(v=4, m=1, b=8, g=128), seed=11)
     x = cuda_x(orc.bench_input_array(4096, 1, 3))
     for u in (1, 2, 4):
-        ref = cg.DeviceLayer(q, u=u).gemm(x).cpu().numpy()
-        again = cg.DeviceLayer(q, u=u).gemm(x).cpu().numpy()
+        ref = cg.DeviceLayer(q, u=u, flags=DET).gemm(x).cpu().numpy()
+        again = cg.DeviceLayer(q, u=u, flags=DET).gemm(x).cpu().numpy()
         assert np.array_equal(u32(ref), u32(again))
         for rg in (1, 3, 16, 63):
-            y = cg.DeviceLayer(q, u=u, rg_per_task=rg).gemm(x).cpu().numpy()
+            y = cg.DeviceLayer(q, u=u, rg_per_task=rg, flags=DET).gemm(x).cpu().numpy()
             assert np.array_equal(u32(y), u32(ref)), (u, rg)
+            # default split-K (L2 reduce-add): same values up to fp32 add order
+            y2 = cg.DeviceLayer(q, u=u, rg_per_task=rg).gemm(x).cpu().numpy()
+            assert_within_tolerance(y2, ref, f"reduce-add u={u} rg={rg}")
 
 
 def test_row_shards_bit_identical_to_full_layer():
     q = cg.random_layer(1000, 2048, cg.QuantConfig(v=8, m=2, b=8, g=128), seed=12)
     x = cuda_x(orc.bench_input_array(2048, 1, 4))
-    full = cg.DeviceLayer(q, u=2).gemm(x).cpu().numpy()
+    full = cg.DeviceLayer(q, u=2, flags=DET).gemm(x).cpu().numpy()
     bounds = [0, 250, 500, 750, 1000]
-    parts = [cg.DeviceLayer(q, u=2, row_range=(a, b)).gemm(x).cpu().numpy()
+    parts = [cg.DeviceLayer(q, u=2, row_range=(a, b), flags=DET).gemm(x).cpu().numpy()
              for a, b in zip(bounds, bounds[1:])]
     assert np.array_equal(u32(np.concatenate(parts)), u32(full))
 
@@ -218,7 +226,7 @@ def test_strict_independent_of_tiling():
 def test_host_and_device_entry_points_agree():
     q = cg.random_layer(300, 1024, cg.QuantConfig(v=4, m=1, b=8, g=128), seed=9)
     x = orc.bench_input_array(1024, 2, 9)
-    dl = cg.DeviceLayer(q)
+    dl = cg.DeviceLayer(q, flags=DET)
     y_host = dl.gemm_host(x)
     y_dev = dl.gemm(cuda_x(x)).cpu().numpy()
     assert np.array_equal(u32(y_host), u32(y_dev))
@@ -245,3 +253,46 @@ def test_fast_mode_rejected_when_unsupported():
     assert not dl.info["fast_supported"]
     with pytest.raises(cg.ConfigError):
         dl.gemm_host(np.ones((128, 1), np.float16), mode="fast")
+
+
+def test_group_launch_bit_identical_to_single_launches():
+    shapes = [(300, 1024), (4096, 512), (37, 2048), (1000, 4096), (64, 128)]
+    layers, xs, refs = [], [], []
+    for i, (r, c) in enumerate(shapes):
+        q = cg.random_layer(r, c, cg.QuantConfig(v=4, m=1, b=8, g=128), seed=40 + i)
+        dl = cg.DeviceLayer(q, flags=DET)
+        x = cuda_x(orc.bench_input_array(c, 2, i))
+        layers.append(dl)
+        xs.append(x)
+        refs.append(dl.gemm(x).cpu().numpy())
+    ys = cg.gemm_group(layers, xs)
+    for y, ref in zip(ys, refs):
+        assert np.array_equal(u32(y.cpu().numpy()), u32(ref))
+    # and again (tickets are monotonic across calls)
+    ys = cg.gemm_group(layers, xs)
+    for y, ref in zip(ys, refs):
+        assert np.array_equal(u32(y.cpu().numpy()), u32(ref))
+
+
+def test_repeated_calls_stable():
+    q = cg.random_layer(2000, 8192, cg.QuantConfig(v=8, m=2, b=8, g=128), seed=77)
+    dl = cg.DeviceLayer(q, flags=DET)
+    x = cuda_x(orc.bench_input_array(8192, 1, 5))
+    ref = dl.gemm(x).cpu().numpy()
+    for _ in range(5):
+        assert np.array_equal(u32(dl.gemm(x).cpu().numpy()), u32(ref))
+
+
+def test_group_launch_default_mode_within_tolerance():
+    layers, xs, refs = [], [], []
+    for i, (r, c) in enumerate([(4096, 4096), (14336, 4096), (4096, 14336)]):
+        q = cg.random_layer(r, c, cg.QuantConfig(v=4, m=1, b=8, g=128), seed=90 + i)
+        x16 = orc.bench_input_array(c, 1, i)
+        layers.append(cg.DeviceLayer(q))
+        xs.append(cuda_x(x16))
+        refs.append(c_oracle.codegemm([p.codes for p in q.planes], [b.entries for b in q.books],
+                                      q.scales.scales, x16, 4, 128, threads=8))
+    for _ in range(3):
+        ys = cg.gemm_group(layers, xs)
+        for y, ref in zip(ys, refs):
+            assert_within_tolerance(y.cpu().numpy(), ref, "group reduce-add")

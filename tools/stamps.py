@@ -29,7 +29,7 @@ _lib.check(lib.cg_debug_stamps(dl.handle, buf.ctypes.data, n * 8))
 st = buf.reshape(n, 8).astype(np.int64)
 t0 = st[:, 0].min()
 rel = (st - t0) / 1000.0  # us
-names = ["start", "x+books staged", "built", "gathered", "barrier", "end", "dummy"]
+names = ["start", "loads+fixups", "built", "gathered", "end"]
 print(dl.info)
 for k, nm in enumerate(names):
     col = rel[:, k]
