@@ -329,6 +329,7 @@ int launch_same_u(cg_layer* const* layers, const uint16_t* const* xs, float* con
     gp.list_cap = cap;
     gp.zero_ticket = layers[0]->zero_ticket;
     if (layers[0]->flags & CG_OPT_DETERMINISTIC) gp.flags |= cg::kFlagDeterministic;
+    if (const char* e = std::getenv("CG_DEBUG_FLAGS")) gp.flags |= std::atoi(e);
     const bool pdl = !(layers[0]->flags & CG_OPT_NO_PDL);
     CG_CUDA(cg::launch_group_gemv(p0.v, p0.m, p0.u, p0.kbits, gp, grid, lay.total, pdl, s),
             "fused gemv launch");

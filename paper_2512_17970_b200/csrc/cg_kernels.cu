@@ -206,8 +206,10 @@ struct FusedShape {
     static constexpr int kPsumFloats = kRegions * kRegionFloats;
     static constexpr int kBookFloats = M * kCodes * V * 2;          // duplicated pairs
     static constexpr int kSliceSegs = 32 * U;
-    static constexpr int kXRow = kSliceSegs + kSliceSegs / (4 * U);  // skewed row
-    static constexpr int kXFloats = V * kXRow;
+    // x staged pre-paired for FFMA2 (see x_pair_index): per u, per lane quad q,
+    // 2V float2 pairs, plus a 16-byte skew per q (conflict-free 128-bit loads)
+    static constexpr int kXQuad = 4 * V + 4;  // floats per (u, q) incl. skew pad
+    static constexpr int kXFloats = U * 8 * kXQuad;
     static constexpr int kPsumBytes = 4 * kPsumFloats;
     static constexpr int kBookBytes = 4 * kBookFloats;
     static constexpr int kXBytes = 4 * kXFloats;
@@ -216,10 +218,15 @@ struct FusedShape {
     static constexpr int kXPerThread = (V * kSliceSegs + kThreads - 1) / kThreads;
 };
 
+// Element k of slice segment s lives in the pair (x_{s0,k}, x_{s1,k}) with
+// s0,s1 = segments of lanes 4q+2h, 4q+2h+1 at the same u: the build thread of
+// quad q loads its 2V pairs with V 128-bit loads into aligned register pairs.
 template <int V, int M, int U, int KB>
-__device__ __forceinline__ int x_slot(int k, int s) {
+__device__ __forceinline__ int x_pair_index(int s, int k) {
     using S = FusedShape<V, M, U, KB>;
-    return k * S::kXRow + s + s / (4 * U);
+    const int l = s / U, u = s - (s / U) * U;
+    const int q = l >> 2, i = l & 3, h = i >> 1, lo = i & 1;
+    return (u * 8 + q) * S::kXQuad + ((h * V + k) << 1) + lo;
 }
 
 // Load this thread's share of the codebooks (binary16) into registers.
@@ -274,7 +281,7 @@ __device__ __forceinline__ void store_x(float* x32,
 #pragma unroll
     for (int i = 0; i < S::kXPerThread; ++i) {
         const int l = tid + i * kThreads;
-        if (l < S::kSliceSegs * V) x32[x_slot<V, M, U, KB>(l % V, l / V)] = h2f(r[i]);
+        if (l < S::kSliceSegs * V) x32[x_pair_index<V, M, U, KB>(l / V, l % V)] = h2f(r[i]);
     }
 }
 
@@ -285,39 +292,69 @@ __device__ __forceinline__ void build_psumbook_smem(float* psum, const float2* b
     const int lane = tid & 31, warp = tid >> 5;
     const int q = lane & 7;     // this thread writes lanes 4q..4q+3 of a code row
     const int csub = lane >> 3; // 4 codes per warp per pass
+    // codes this thread owns: c0 + 64*i; all of them in flight at once when the
+    // table is full size (kcount == 2**KB): 2*CPT independent FFMA2 chains
+    constexpr int kCPT = S::kCodes / (4 * kWarps) > 0 ? S::kCodes / (4 * kWarps) : 1;
+    const int c0 = csub + 4 * warp;
 #pragma unroll 1
     for (int j = 0; j < S::kSub; ++j) {
         const int t = j / U, uu = j % U;
+        // x of this thread's 4 segments, already paired for FFMA2:
+        // x01[k] = (x_s0k, x_s1k), x23[k] = (x_s2k, x_s3k)
         float2 x01[V], x23[V];
+        {
+            const float4* src = reinterpret_cast<const float4*>(x32 + (uu * 8 + q) * S::kXQuad);
 #pragma unroll
-        for (int k = 0; k < V; ++k) {
-            const int s0 = (4 * q) * U + uu;
-            x01[k] = make_float2(x32[x_slot<V, M, U, KB>(k, s0)],
-                                 x32[x_slot<V, M, U, KB>(k, s0 + U)]);
-            x23[k] = make_float2(x32[x_slot<V, M, U, KB>(k, s0 + 2 * U)],
-                                 x32[x_slot<V, M, U, KB>(k, s0 + 3 * U)]);
+            for (int c = 0; c < V; ++c) {  // 2V pairs = V float4
+                const float4 w = src[c];
+                float2* dstp = (2 * c < V) ? &x01[2 * c] : &x23[2 * c - V];
+                dstp[0] = make_float2(w.x, w.y);
+                dstp[1] = make_float2(w.z, w.w);
+            }
         }
         float* dst = psum + (j >> 1) * S::kRegionFloats + (j & 1) * 32 + q * 4;
         const float2* bk = books2 + t * S::kCodes * V;
-        // two codes per iteration: four independent FFMA2 chains in flight
-#pragma unroll 1
-        for (int c = csub + 4 * warp; c < kcount; c += 8 * kWarps) {
-            const int c2 = c + 4 * kWarps;
-            const bool has2 = c2 < kcount;
-            float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
-            float2 b01 = make_float2(0.0f, 0.0f), b23 = make_float2(0.0f, 0.0f);
+        if (kcount == S::kCodes && kCPT * 4 * kWarps == S::kCodes) {
+            float2 cc[kCPT][V];
 #pragma unroll
-            for (int k = 0; k < V; ++k) {
-                const float2 ca = bk[c * V + k];
-                const float2 cb = bk[(has2 ? c2 : c) * V + k];
-                a01 = __ffma2_rn(ca, x01[k], a01);
-                a23 = __ffma2_rn(ca, x23[k], a23);
-                b01 = __ffma2_rn(cb, x01[k], b01);
-                b23 = __ffma2_rn(cb, x23[k], b23);
+            for (int i = 0; i < kCPT; ++i) {
+                const float4* src = reinterpret_cast<const float4*>(bk + (c0 + 4 * kWarps * i) * V);
+#pragma unroll
+                for (int k = 0; k < V; k += 2) {
+                    const float4 w = src[k / 2];
+                    cc[i][k] = make_float2(w.x, w.y);
+                    if (k + 1 < V) cc[i][k + 1] = make_float2(w.z, w.w);
+                }
             }
-            *reinterpret_cast<float4*>(dst + c * 64) = make_float4(a01.x, a01.y, a23.x, a23.y);
-            if (has2)
-                *reinterpret_cast<float4*>(dst + c2 * 64) = make_float4(b01.x, b01.y, b23.x, b23.y);
+            float2 a01[kCPT], a23[kCPT];
+#pragma unroll
+            for (int i = 0; i < kCPT; ++i) {
+                a01[i] = make_float2(0.0f, 0.0f);
+                a23[i] = make_float2(0.0f, 0.0f);
+            }
+#pragma unroll
+            for (int k = 0; k < V; ++k)
+#pragma unroll
+                for (int i = 0; i < kCPT; ++i) {
+                    a01[i] = __ffma2_rn(cc[i][k], x01[k], a01[i]);
+                    a23[i] = __ffma2_rn(cc[i][k], x23[k], a23[i]);
+                }
+#pragma unroll
+            for (int i = 0; i < kCPT; ++i)
+                *reinterpret_cast<float4*>(dst + (c0 + 4 * kWarps * i) * 64) =
+                    make_float4(a01[i].x, a01[i].y, a23[i].x, a23[i].y);
+        } else {
+#pragma unroll 1
+            for (int c = c0; c < kcount; c += 4 * kWarps) {
+                float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    const float2 cc = bk[c * V + k];
+                    a01 = __ffma2_rn(cc, x01[k], a01);
+                    a23 = __ffma2_rn(cc, x23[k], a23);
+                }
+                *reinterpret_cast<float4*>(dst + c * 64) = make_float4(a01.x, a01.y, a23.x, a23.y);
+            }
         }
     }
 }
@@ -701,8 +738,10 @@ __device__ __forceinline__ void run_task(const GroupParams& p, int l, int64_t ta
         }
         store_x<V, M, U, KB>(x32, xreg, tid);
         __syncthreads();
+        if (col == 0) CG_STAMP(5)
         build_psumbook_smem<V, M, U, KB>(psum, books2, x32, L.kcount, tid);
         __syncthreads();
+        if (p.flags & 512) continue;  // diagnostics: prologue + build only
         if (my_rgs > 0) load_tile<V, M, U, KB>(bufA, cptr);
         if (col == 0) {
             CG_STAMP(2)

@@ -29,7 +29,7 @@ _lib.check(lib.cg_debug_stamps(dl.handle, buf.ctypes.data, n * 8))
 st = buf.reshape(n, 8).astype(np.int64)
 t0 = st[:, 0].min()
 rel = (st - t0) / 1000.0  # us
-names = ["start", "loads+fixups", "built", "gathered", "end"]
+names = ["start", "loads+fixups", "built", "gathered", "end", "x staged"]
 print(dl.info)
 for k, nm in enumerate(names):
     col = rel[:, k]
@@ -38,6 +38,10 @@ for k, nm in enumerate(names):
         print(f"{nm:16s} min {col.min():7.2f}  median {np.median(col):7.2f}  max {col.max():7.2f} us")
 d = rel[:, 3] - rel[:, 2]
 print(f"gather duration: min {d.min():.2f} median {np.median(d):.2f} max {d.max():.2f} us")
+d = rel[:, 2] - rel[:, 5]
+print(f"build only: min {d.min():.2f} median {np.median(d):.2f} max {d.max():.2f} us")
+d = rel[:, 5] - rel[:, 1]
+print(f"x wait: min {d.min():.2f} median {np.median(d):.2f} max {d.max():.2f} us")
 d = rel[:, 2] - rel[:, 1]
 print(f"build duration: min {d.min():.2f} median {np.median(d):.2f} max {d.max():.2f} us")
 d = rel[:, 1] - rel[:, 0]
