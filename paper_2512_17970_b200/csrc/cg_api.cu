@@ -71,6 +71,15 @@ int scale_lg(const cg::Plan& p, int u) {
     return ilog2(lanes);
 }
 
+// Raw task inputs staged by bulk copy: binary16 codebooks, then (16-byte
+// aligned) the binary16 x slice of one task.
+int raw_books_bytes(const cg::Plan& p) { return (p.m * p.kcount * p.v * 2 + 15) / 16 * 16; }
+int raw_input_bytes(const cg::Plan& p, int u) { return raw_books_bytes(p) + 32 * u * p.v * 2; }
+// fix-up list entries (deterministic) or the split-K staging rows (reduce-add)
+int list_bytes_for(int64_t rg_per_task, int n) {
+    return (int)std::max((rg_per_task * n + 16) * 16, rg_per_task * 16 * n * 4);
+}
+
 // Planner: pick u (segments per lane) and rows per task for the fused kernel.
 // Cost model per SM, in shared-memory wavefronts (the co-bound with HBM):
 //   gather  = rows/16 * 16*(u*m + 1)   (one LDS per lookup + SHFL reduction)
@@ -94,6 +103,7 @@ void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms, int reserved) {
         cg::FusedSizes z;
         if (!cg::fused_sizes(p.v, p.m, u, p.kbits, &z)) continue;
         const int n_gs = 32 >> lg;
+        const int raw_bytes = raw_input_bytes(p, u);
         // rows per task are capped by the smem left for the task's scale tiles
         int64_t rg_cap = 0;
         {
@@ -101,8 +111,8 @@ void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms, int reserved) {
             int64_t lo = 0, hi = 1 << 16;
             while (lo < hi) {  // largest rg count whose layout fits
                 const int64_t mid = (lo + hi + 1) / 2;
-                if (cg::smem_layout(z, (int)(mid * n_gs * 32), (int)(mid + 32) * 16, reserved,
-                                    &lay))
+                if (cg::smem_layout(z, (int)(mid * n_gs * 32), raw_bytes, list_bytes_for(mid, 1),
+                                    reserved, &lay, (int)(mid * 64)))
                     lo = mid;
                 else hi = mid - 1;
             }
@@ -126,8 +136,8 @@ void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms, int reserved) {
         const int64_t n_rb = (n_rg + rg_per_task - 1) / rg_per_task;
         const int64_t tasks = n_slices * n_rb;
         cg::SmemLayout lay;
-        cg::smem_layout(z, (int)(rg_per_task * n_gs * 32), (int)(rg_per_task + 32) * 16, reserved,
-                        &lay);
+        cg::smem_layout(z, (int)(rg_per_task * n_gs * 32), raw_bytes,
+                        list_bytes_for(rg_per_task, 1), reserved, &lay, (int)(rg_per_task * 64));
         const double per_task = (double)rg_per_task * 16.0 * (u * p.m + 1) +
                                 (double)p.m * u * (1 << p.kbits) + 600.0;
         const double waves = std::ceil((double)tasks / ((double)sms * occ));
@@ -313,21 +323,37 @@ int launch_same_u(cg_layer* const* layers, const uint16_t* const* xs, float* con
     // fix-up list / owned-ticket targets (deterministic) or the staging buffer
     // of a task's partial rows (reduce-add): the larger of the two
     const int cap = rg_max * n + 16;
-    const int list_bytes = std::max(cap * 16, rg_max * 16 * n * 4);
+    const int list_bytes = (int)list_bytes_for(rg_max, n);
+    int raw_bytes = 0, books_raw = 0;
+    bool x_copy = (n == 1);
+    for (int i = 0; i < count; ++i) {
+        const cg::Plan& p = layers[i]->plan;
+        raw_bytes = std::max(raw_bytes, raw_input_bytes(p, p.u));
+        books_raw = std::max(books_raw, raw_books_bytes(p));
+        // x travels by bulk copy only if every slice of it is a 16-byte multiple
+        if ((reinterpret_cast<uintptr_t>(xs[i]) & 15) || (p.cols % 8)) x_copy = false;
+    }
     cg::SmemLayout lay;
-    if (!cg::smem_layout(zmax, scl_max, list_bytes, layers[0]->reserved, &lay))
+    if (!cg::smem_layout(zmax, scl_max, raw_bytes, list_bytes, layers[0]->reserved, &lay,
+                         rg_max * 16 * n * 4))
         return fail(CG_ERR_CONFIG,
                     "fused kernel does not fit in shared memory at n=%d (rows per task %d); "
                     "use fewer columns per call or CG_MODE_STRICT", n, rg_max);
     gp.off_psum = lay.off_psum;
     gp.off_books = lay.off_books;
     gp.off_x = lay.off_x;
-    gp.off_scl = lay.off_scl;
+    gp.off_scl[0] = lay.off_scl[0];
+    gp.off_scl[1] = lay.off_scl[1];
+    gp.off_raw[0] = lay.off_raw[0];
+    gp.off_raw[1] = lay.off_raw[1];
+    gp.raw_x_off = books_raw;
     gp.off_bar = lay.off_bar;
     gp.off_list = lay.off_list;
-    gp.off_stage = lay.off_list;
+    gp.off_stage[0] = lay.off_list;
+    gp.off_stage[1] = lay.off_stage1;
     gp.list_cap = cap;
     gp.zero_ticket = layers[0]->zero_ticket;
+    if (!x_copy) gp.flags |= cg::kFlagXRegs;
     if (layers[0]->flags & CG_OPT_DETERMINISTIC) gp.flags |= cg::kFlagDeterministic;
     if (const char* e = std::getenv("CG_DEBUG_FLAGS")) gp.flags |= std::atoi(e);
     const bool pdl = !(layers[0]->flags & CG_OPT_NO_PDL);
@@ -525,9 +551,8 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
         cudaMemset(L->zero_ticket, 0, 16);
     }
     if (p.fast && std::getenv("CG_STAMPS")) {
-        if ((rc = dev_alloc(L, &L->stamps, (size_t)p.n_slices * p.n_rb * 64, "stamps")))
-            return bail(rc);
-        cudaMemset(L->stamps, 0, (size_t)p.n_slices * p.n_rb * 64);
+        if ((rc = dev_alloc(L, &L->stamps, (size_t)L->sms * 256, "stamps"))) return bail(rc);
+        cudaMemset(L->stamps, 0, (size_t)L->sms * 256);
     }
     *out = L;
     return CG_OK;
@@ -668,7 +693,7 @@ int cg_psumbook_build(const void* books, const void* x, int m, int b, int v, int
 extern "C" int cg_debug_stamps(cg_layer* L, unsigned long long* host, int64_t count) {
     if (!L || !L->stamps) return fail(CG_ERR_ARG, "no stamps (set CG_STAMPS=1)");
     DeviceGuard guard(L->device);
-    const int64_t n = std::min<int64_t>(count, L->plan.n_slices * L->plan.n_rb * 8);
+    const int64_t n = std::min<int64_t>(count, (int64_t)L->sms * 32);
     CG_CUDA(cudaMemcpy(host, L->stamps, n * 8, cudaMemcpyDeviceToHost), "stamps D2H");
     return CG_OK;
 }

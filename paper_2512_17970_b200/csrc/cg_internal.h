@@ -50,8 +50,10 @@ struct GroupParams {
     int flags, pf_dist;
     // dynamic shared-memory layout (bytes from the dynamic smem start); the
     // Psumbook sits at a 64 KB-aligned shared-window address (see cg_api.cu)
-    int off_psum, off_books, off_x, off_scl, off_bar, off_list, list_cap;
-    int off_stage;            // split-K staging of a task's partial rows (atomic mode)
+    int off_psum, off_books, off_x, off_bar, off_list, list_cap;
+    int off_scl[2], off_raw[2];  // double-buffered task inputs: scale tiles, raw books | x
+    int raw_x_off;            // byte offset of the raw x slice inside a raw buffer
+    int off_stage[2];         // split-K staging of a task's partial rows (reduce-add), x2
     unsigned long long* zero_ticket;  // {count, generation}: every CTA zeroed its share of y
     unsigned long long* stamps;  // diagnostics: per-CTA phase timestamps (8 per CTA) or null
 };
@@ -69,6 +71,7 @@ struct DumpParams {
 constexpr int kFlagNoPrefetch = 2;
 constexpr int kFlagLastArriver = 4;  // a layer has more tasks than the grid: last arriver sums
 constexpr int kFlagDeterministic = 16;  // split-K by tickets + ordered sums (else L2 reduce-add)
+constexpr int kFlagXRegs = 32;  // x staged through registers (unaligned x / odd cols / n > 1)
 
 // shared-memory pieces of the fused kernel for (v, m, u, kbits)
 struct FusedSizes {
@@ -81,35 +84,58 @@ bool fused_sizes(int v, int m, int u, int kbits, FusedSizes* out);
 // the CTA's shared window so that one PRMT builds a whole lookup address; the
 // dynamic area starts `reserved` bytes into the window (1 KB on sm_100).
 struct SmemLayout {
-    int off_psum = 0, off_books = 0, off_x = 0, off_scl = 0, off_bar = 0, off_list = 0, total = 0;
+    int off_psum = 0, off_books = 0, off_x = 0, off_bar = 0, off_list = 0, total = 0;
+    int off_scl[2] = {0, 0}, off_raw[2] = {0, 0}, off_stage1 = 0;
 };
-// list_bytes covers the fix-up list (deterministic mode) or the split-K
-// staging buffer (reduce-add mode), whichever is larger
-inline bool smem_layout(const FusedSizes& z, int scl_bytes, int list_bytes, int reserved,
-                        SmemLayout* L) {
+// Pieces go first-fit into the area below the 64 KB-aligned Psumbook (the
+// dynamic area starts `reserved` bytes into the CTA window), the rest after it.
+//   scl_bytes / raw_bytes: one task-input buffer (two of each are placed)
+//   list_bytes: fix-up list (deterministic) or split-K staging (reduce-add);
+//   a second staging buffer of stage_bytes is placed for the reduce-add flush
+inline bool smem_layout(const FusedSizes& z, int scl_bytes, int raw_bytes, int list_bytes,
+                        int reserved, SmemLayout* L, int stage_bytes = 0) {
     auto up = [](int v, int a) { return (v + a - 1) / a * a; };
     const int kMax = 227 * 1024;
-    int low = 0;
-    L->off_x = low;
-    low = up(low + z.x, 16);
-    L->off_scl = low;
-    low = up(low + scl_bytes, 16);
-    L->off_list = low;
-    low = up(low + list_bytes, 16);
-    L->off_bar = low;
-    low = up(low + 64, 16);  // CtaState: mbarrier, fix-up count, previous task, grid gen
-    const int gap = up(reserved + low, 65536) - reserved;  // first aligned slot
-    if (gap - low >= z.books) {                           // books fit below
-        L->off_books = low;
-        L->off_psum = gap;
-        L->total = gap + z.psum;
-    } else {
-        L->off_psum = gap;
-        L->off_books = gap + z.psum;
-        L->total = L->off_books + z.books;
+    const int kState = 128;  // CtaState
+    struct Piece {
+        int* off;
+        int size;
+    } pieces[] = {{&L->off_books, z.books},       {&L->off_list, list_bytes},
+                  {&L->off_scl[0], scl_bytes},    {&L->off_scl[1], scl_bytes},
+                  {&L->off_raw[0], raw_bytes},    {&L->off_raw[1], raw_bytes},
+                  {&L->off_x, z.x},               {&L->off_bar, kState},
+                  {&L->off_stage1, stage_bytes}};
+    const int n = (int)(sizeof(pieces) / sizeof(pieces[0]));
+    // largest first
+    for (int i = 0; i < n; ++i)
+        for (int j = i + 1; j < n; ++j)
+            if (pieces[j].size > pieces[i].size) {
+                Piece t = pieces[i];
+                pieces[i] = pieces[j];
+                pieces[j] = t;
+            }
+    int total_small = 0;
+    for (int i = 0; i < n; ++i) total_small += up(pieces[i].size, 16);
+    // the Psumbook's first 64 KB-aligned slot; grow past it if nothing fits below
+    const int gap = up(reserved + 1, 65536) - reserved;
+    int low = 0, high = gap + z.psum;
+    L->off_psum = gap;
+    for (int i = 0; i < n; ++i) {
+        const int sz = up(pieces[i].size, 16);
+        if (low + sz <= gap) {
+            *pieces[i].off = low;
+            low += sz;
+        } else {
+            *pieces[i].off = high;
+            high += sz;
+        }
     }
+    (void)total_small;
+    L->total = high;
     return L->total <= kMax;
 }
+
+
 struct Plan {
     int64_t rows = 0, cols = 0, segs = 0, g_eff = 0, groups = 0;
     int v = 0, m = 0, b = 0, kcount = 0;

@@ -453,6 +453,10 @@ __device__ __forceinline__ void bulk_reduce_add_f32(float* dst, const float* src
 __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+// all but the most recent bulk group have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read_prev() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_all() {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -580,9 +584,9 @@ struct FixupEntry {
 // next task, after that task's input loads are in flight, or at kernel end)
 // and the zero-barrier generation.
 struct CtaState {
-    uint64_t scl_bar;             // mbarrier of the scale-tile bulk copy
+    uint64_t in_bar[2];           // mbarriers of the two task-input buffers
     int list_count;
-    unsigned bar_phase;
+    unsigned in_phase;            // parity bit per input buffer
     unsigned long long zero_gen;  // grid generation seen at arrival
     int zero_ready;
     int prev_layer;
@@ -663,58 +667,122 @@ __device__ void close_task(const GroupParams& p, unsigned char* smem_raw, int ti
     if (tid == 0) *list_count = 0;
 }
 
-// reduce-add mode: the first split-K flush of a CTA waits until every CTA
-// has zeroed its share of the outputs (grid ticket taken at kernel start)
+// ---- task inputs: raw codebooks + x slice + scale tiles by TMA bulk copies
+// into one of two smem buffers (double-buffered across tasks), so the next
+// task's inputs travel while the current task gathers.
+struct TaskCoord {
+    int l;
+    int64_t t;
+};
+
+__device__ __forceinline__ bool next_task(const GroupParams& p, TaskCoord& c) {
+    c.t += gridDim.x;
+    while (c.l < p.n_layers && c.t >= p.layer[c.l].n_tasks) {
+        ++c.l;
+        c.t = blockIdx.x;
+    }
+    return c.l < p.n_layers;
+}
+
+__device__ __forceinline__ bool x_by_copy(const GroupParams& p) {
+    return p.n == 1 && !(p.flags & kFlagXRegs);
+}
+
+// tid 0 only.  weights: scale tiles + codebooks; x: the slice of x (n == 1).
 template <int V, int M, int U, int KB>
-__device__ __forceinline__ void run_task(const GroupParams& p, int l, int64_t task, bool first_task,
-                                         unsigned char* smem_raw, int tid) {
+__device__ __forceinline__ void issue_inputs(const GroupParams& p, TaskCoord c, int buf,
+                                             unsigned char* smem_raw, bool weights, bool x) {
     using S = FusedShape<V, M, U, KB>;
+    const LayerTask& L = p.layer[c.l];
+    CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
+    const int64_t slice = (int)c.t / (int)L.n_rb;
+    const int64_t rb = (int)c.t - (int)slice * (int)L.n_rb;
+    const int64_t rg0 = rb * L.rg_per_task;
+    const int64_t rg1 = min(rg0 + (int64_t)L.rg_per_task, L.n_rg);
+    const uint32_t scl_bytes = (uint32_t)((rg1 - rg0) * L.n_gs * 32);
+    const uint32_t book_bytes = (uint32_t)((M * L.kcount * V * 2 + 15) & ~15);  // alloc is padded
+    const int64_t e0 = slice * (int64_t)(S::kSliceSegs * V);
+    const int64_t xn = min((int64_t)(S::kSliceSegs * V), L.cols - e0);
+    const uint32_t x_bytes = x_by_copy(p) ? (uint32_t)(xn * 2) : 0u;  // host: 16-B multiple
+    uint64_t* bar = &cs.in_bar[buf];
+    unsigned char* raw = smem_raw + p.off_raw[buf];
+    if (weights) {
+        mbar_expect_tx(bar, scl_bytes + book_bytes + x_bytes);
+        bulk_g2s(smem_raw + p.off_scl[buf], L.scl + (slice * L.n_rg + rg0) * L.n_gs * 16,
+                 scl_bytes, bar);
+        bulk_g2s(raw, L.books, book_bytes, bar);
+    }
+    if (x && x_bytes) bulk_g2s(raw + p.raw_x_off, L.x + e0, x_bytes, bar);
+}
+
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int buf, bool first_task,
+                                         bool has_next, TaskCoord nc, unsigned char* smem_raw,
+                                         int tid, int task_idx) {
+    using S = FusedShape<V, M, U, KB>;
+    const int l = c.l;
+    const int64_t task = c.t;
     const LayerTask& L = p.layer[l];
     float* psum = reinterpret_cast<float*>(smem_raw + p.off_psum);
     float2* books2 = reinterpret_cast<float2*>(smem_raw + p.off_books);
     float* x32 = reinterpret_cast<float*>(smem_raw + p.off_x);
-    uint16_t* scl_s = reinterpret_cast<uint16_t*>(smem_raw + p.off_scl);
+    const uint16_t* scl_s = reinterpret_cast<const uint16_t*>(smem_raw + p.off_scl[buf]);
+    const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem_raw + p.off_raw[buf]);
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
-    uint64_t* scl_bar = &cs.scl_bar;
     unsigned long long* stamps =
-        (p.stamps && first_task && l == 0) ? p.stamps + blockIdx.x * 8 : nullptr;
+        (p.stamps && task_idx < 3) ? p.stamps + blockIdx.x * 32 + task_idx * 8 : nullptr;
 #define CG_STAMP(k) \
     if (stamps && tid == 0) stamps[k] = gtimer();
 
     const int lane = tid & 31, warp = tid >> 5;
     const int n = p.n;
-    const int64_t slice = task / L.n_rb;
-    const int64_t rb = task - slice * L.n_rb;
-    const int64_t rg0 = rb * L.rg_per_task;
+    const int slice = (int)task / (int)L.n_rb;  // task counts fit in 32 bits
+    const int rb = (int)task - slice * (int)L.n_rb;
+    const int64_t rg0 = (int64_t)rb * L.rg_per_task;
     const int64_t rg1 = min(rg0 + (int64_t)L.rg_per_task, L.n_rg);
     const int n_gs = L.n_gs;
-    const uint8_t* tiles = L.codes + slice * L.n_rg * (int64_t)S::kTileBytes;
+    const uint8_t* tiles = L.codes + (int64_t)slice * L.n_rg * (int64_t)S::kTileBytes;
     const bool split = L.n_slices > 1;
     CG_STAMP(0)
 
-    // 1. inputs of this task in flight: codebooks, x (column 0), first tiles -> L2
+    // 1. this task's first code tiles towards L2 (codebooks, x and scales were
+    //    put in flight one task earlier, or before griddepcontrol.wait)
     const int my_rgs = rg0 + warp < rg1 ? (int)((rg1 - rg0 - warp + kWarps - 1) / kWarps) : 0;
     const uint8_t* cptr = tiles + (rg0 + warp) * S::kTileBytes + lane * 16;
     constexpr int64_t kStep = (int64_t)kWarps * S::kTileBytes;
     const uint8_t* wtile = tiles + (rg0 + warp) * S::kTileBytes;
     const int pf = (p.flags & kFlagNoPrefetch) ? 0 : p.pf_dist;
-    if (lane < 2 + pf && lane < my_rgs) prefetch_l2_bulk(wtile + lane * kStep, S::kTileBytes);
-    uint16_t breg[S::kBookPerThread];
-    load_books<V, M, U, KB>(breg, L.books, L.kcount, tid);
+    if (!(p.flags & kFlagNoPrefetch) && lane < 2 + pf && lane < my_rgs)
+        prefetch_l2_bulk(wtile + lane * kStep, S::kTileBytes);
     uint16_t xreg[S::kXPerThread];
-    load_x<V, M, U, KB>(xreg, L.x, slice, L.cols, n, 0, tid);
+    if (!x_by_copy(p)) load_x<V, M, U, KB>(xreg, L.x, slice, L.cols, n, 0, tid);
 
-    // 2. the previous task is done with tables, scales and the staging buffer;
-    //    close its row groups
-    if (tid == 0) bulk_wait_read();
+    // 2. the previous task is done with the table; the staging buffer of two
+    //    tasks ago has been read by its flush; close the previous task's row
+    //    groups (deterministic mode); the next task's inputs start travelling
+    if (tid == 0) bulk_wait_read_prev();
     __syncthreads();
-    if (tid == 0) {
-        const uint32_t bytes = (uint32_t)((rg1 - rg0) * n_gs * 32);
-        mbar_expect_tx(scl_bar, bytes);
-        bulk_g2s(scl_s, L.scl + (slice * L.n_rg + rg0) * n_gs * 16, bytes, scl_bar);
-    }
+    CG_STAMP(7)
+    if (tid == kThreads - 32 && has_next)
+        issue_inputs<V, M, U, KB>(p, nc, buf ^ 1, smem_raw, true, true);
     close_task(p, smem_raw, tid);
-    store_books<V, M, U, KB>(books2, breg, L.kcount, tid);
+    mbar_wait(&cs.in_bar[buf], (cs.in_phase >> buf) & 1u);
+    CG_STAMP(4)
+    // raw binary16 codebooks -> duplicated binary32 pairs
+    if (L.kcount == S::kCodes) {  // full-size tables: same index, two halves per thread
+        const uint32_t* raw2 = reinterpret_cast<const uint32_t*>(raw);
+        float4* b4 = reinterpret_cast<float4*>(books2);
+        for (int e = tid; e < M * S::kCodes * V / 2; e += kThreads) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&raw2[e]));
+            b4[e] = make_float4(f.x, f.x, f.y, f.y);
+        }
+    } else {
+        for (int e = tid; e < M * L.kcount * V; e += kThreads) {
+            const int t = e / (L.kcount * V);
+            const float f = h2f(raw[e]);
+            books2[t * S::kCodes * V + (e - t * L.kcount * V)] = make_float2(f, f);
+        }
+    }
     CG_STAMP(1)
 
     // per-lane constants of the gather (Psumbook base must be 64 KB aligned)
@@ -736,20 +804,26 @@ __device__ __forceinline__ void run_task(const GroupParams& p, int l, int64_t ta
             __syncthreads();  // previous column's table is no longer read
             load_x<V, M, U, KB>(xreg, L.x, slice, L.cols, n, col, tid);
         }
-        store_x<V, M, U, KB>(x32, xreg, tid);
+        if (x_by_copy(p)) {
+            // raw binary16 x slice (zero past the layer's last column)
+            const uint16_t* xr = raw + p.raw_x_off / 2;
+            const int64_t e0 = slice * (int64_t)(S::kSliceSegs * V);
+            for (int e = tid; e < S::kSliceSegs * V; e += kThreads)
+                x32[x_pair_index<V, M, U, KB>(e / V, e % V)] =
+                    (e0 + e < L.cols) ? h2f(xr[e]) : 0.0f;
+        } else {
+            store_x<V, M, U, KB>(x32, xreg, tid);
+        }
         __syncthreads();
         if (col == 0) CG_STAMP(5)
         build_psumbook_smem<V, M, U, KB>(psum, books2, x32, L.kcount, tid);
         __syncthreads();
-        if (p.flags & 512) continue;  // diagnostics: prologue + build only
+        if (col == 0) CG_STAMP(6)
+        if (col == 0 && first_task) pdl_launch_dependents();
         if (my_rgs > 0) load_tile<V, M, U, KB>(bufA, cptr);
-        if (col == 0) {
-            CG_STAMP(2)
-            if (first_task) pdl_launch_dependents();
-            mbar_wait(scl_bar, cs.bar_phase);
-        }
+        if (col == 0) CG_STAMP(2)
         const bool stage_out = split && !(p.flags & kFlagDeterministic);
-        float* out = stage_out ? reinterpret_cast<float*>(smem_raw + p.off_stage) - rg0 * 16 * n
+        float* out = stage_out ? reinterpret_cast<float*>(smem_raw + p.off_stage[buf]) - rg0 * 16 * n
                                : (split ? L.ws + slice * L.rows * n : L.y);
         int64_t row = (rg0 + warp) * 16 + mask;
         const int64_t row_step = (int64_t)kWarps * 16;
@@ -787,7 +861,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, int l, int64_t ta
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 cs.zero_ready = 1;
             }
-            const float* stage = reinterpret_cast<const float*>(smem_raw + p.off_stage);
+            const float* stage = reinterpret_cast<const float*>(smem_raw + p.off_stage[buf]);
             const int64_t r1 = min(rg1 * 16, L.rows);
             const int64_t elems = (r1 - rg0 * 16) * n;
             const int64_t body = elems & ~int64_t(3);  // 16-byte multiple
@@ -797,7 +871,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, int l, int64_t ta
     }
     __syncthreads();
     if (tid == 0) {
-        cs.bar_phase ^= 1u;
+        cs.in_phase ^= (1u << buf);
         cs.prev_layer = (split && (p.flags & kFlagDeterministic)) ? l : -1;
         cs.prev_slice = slice;
         cs.prev_rg0 = rg0;
@@ -813,16 +887,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
+    TaskCoord c{0, (int64_t)blockIdx.x};
+    bool have = true;
+    while (c.l < p.n_layers && c.t >= p.layer[c.l].n_tasks) {
+        ++c.l;
+        c.t = blockIdx.x;
+    }
+    have = c.l < p.n_layers;
     if (tid == 0) {
-        mbar_init(&cs.scl_bar, 1);
+        mbar_init(&cs.in_bar[0], 1);
+        mbar_init(&cs.in_bar[1], 1);
         cs.list_count = 0;
-        cs.bar_phase = 0;
+        cs.in_phase = 0;
         cs.zero_ready = 0;
         cs.prev_layer = -1;
+        // weights of the first task travel before the wait on the previous kernel
+        if (have) issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, true, false);
     }
-    bool first = true;
     // every layer's x (and y, for write-after-read) belongs to earlier work
     pdl_wait();
+    if (tid == 0 && have) issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, false, true);
     if (!(p.flags & kFlagDeterministic)) {
         // zero this CTA's share of every split layer's output, then take the
         // grid ticket (its round trip overlaps the first task)
@@ -858,20 +942,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     // (all layers of a launch share U: the host splits groups by u)
-    for (int l = 0; l < p.n_layers; ++l) {
-        for (int64_t t = blockIdx.x; t < p.layer[l].n_tasks; t += gridDim.x) {
-            run_task<V, M, U, KB>(p, l, t, first, smem_raw, tid);
-            first = false;
-        }
+    int buf = 0, task_idx = 0;
+    bool first = true;
+    while (have) {
+        TaskCoord nc = c;
+        const bool has_next = next_task(p, nc);
+        run_task<V, M, U, KB>(p, c, buf, first, has_next, nc, smem_raw, tid, task_idx++);
+        first = false;
+        buf ^= 1;
+        c = nc;
+        have = has_next;
     }
     // close the last task's row groups; drain the bulk reduce-adds
     __syncthreads();
     close_task(p, smem_raw, tid);
     if (tid == 0) bulk_wait_all();
-    if (p.stamps && tid == 0 && blockIdx.x < p.layer[0].n_tasks) {
-        __syncthreads();
-        p.stamps[blockIdx.x * 8 + 4] = gtimer();
-    }
+    __syncthreads();
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 32 + 31] = gtimer();
 }
 
 // dump the fused kernel's smem Psumbook in _psum_tables layout (m, segs, 2**b, n)
