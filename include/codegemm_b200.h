@@ -62,6 +62,9 @@ extern "C" {
 #define CG_MODE_FAST 1   /* fused Psumbook + code-gather kernel (fp32 accumulate)      */
 #define CG_MODE_STRICT 2 /* reference operation order: bit-identical to codegemm_gemm  */
 
+#define CG_X_F16 0 /* x stored as binary16                                              */
+#define CG_X_F32 1 /* x stored as float32, rounded to binary16 when read (staged chain) */
+
 /* option flags for cg_layer_options.flags */
 #define CG_OPT_NO_PDL 1        /* launch without programmatic dependent launch        */
 #define CG_OPT_NO_L2_PREFETCH 2 /* skip the bulk L2 prefetch of the CTA's code tiles   */
@@ -123,7 +126,7 @@ int cg_layer_query(const cg_layer* layer, cg_layer_info* info);
 int cg_layer_gemm(cg_layer* layer, const void* x, int n, float* y, int mode, void* stream);
 
 /*
- * Grouped launch: y_i = W_i x_i for `count` (1..8) independent layers in ONE
+ * Grouped launch: y_i = W_i x_i for `count` (1..16) independent layers in ONE
  * launch of the fused kernel (e.g. the q/k/v or gate/up projections of a
  * decoder block, which read the same x).  Layers must share v, m, the code
  * width class (b <= 4 or b <= 8) and the device, and must all have
@@ -132,6 +135,24 @@ int cg_layer_gemm(cg_layer* layer, const void* x, int n, float* y, int mode, voi
  */
 int cg_gemm_group(cg_layer* const* layers, const void* const* xs, float* const* ys, int count,
                   int n, void* stream);
+
+/*
+ * Dependency-staged launch: one persistent launch of the fused kernel runs
+ * `count` (1..16) layers in stages; stages[i] is layer i's stage (starts at 0,
+ * non-decreasing, steps of at most 1).  Layers of one stage are independent
+ * (a grouped launch); a stage may read what earlier stages wrote -- e.g. a
+ * decoder-block chain {q} -> {o} -> {gate,up} -> {down}.  x_dtypes[i] (NULL =
+ * all CG_X_F16) says how xs[i] is stored: CG_X_F16 (cols, n) binary16, or
+ * CG_X_F32 (cols, n) float32 -- typically an earlier stage's y in the same
+ * launch -- rounded to binary16 (round-to-nearest-even) as it is read, the
+ * reference's fp16 boundary rounding (cli.py:136).  The kernel's grid barrier
+ * orders a stage's reads after the earlier stages' writes.  Same layer
+ * requirements as cg_gemm_group, plus one tiling u for all layers
+ * (cg_layer_options.u).  Outputs are bit-identical to separate cg_layer_gemm
+ * calls in stage order on the rounded inputs.
+ */
+int cg_gemm_stages(cg_layer* const* layers, const void* const* xs, const int* x_dtypes,
+                   float* const* ys, const int* stages, int count, int n, void* stream);
 
 /* Same with HOST buffers: copies x in, runs, copies y out, synchronises. */
 int cg_layer_gemm_host(cg_layer* layer, const uint16_t* x, int n, float* y, int mode,

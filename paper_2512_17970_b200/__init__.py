@@ -16,6 +16,7 @@ from .engines import (
     closed_form_counters,
     codegemm_gemm,
     gemm_group,
+    gemm_stages,
     phase_split,
 )
 from .errors import (
@@ -49,6 +50,6 @@ __all__ = [
     "DeviceLayer", "DimOverflowError", "FormatError", "IntegrityError", "Matrix", "OpCounters",
     "Psumbook", "QuantConfig", "QuantizedLayer", "ScalePlane", "ShapeError", "TileConfig",
     "TruncatedFileError", "UnsupportedVersionError", "build_psumbook", "closed_form_counters",
-    "codegemm_gemm", "encode_f16_array", "gemm_group", "pack_codes", "phase_split", "random_layer",
+    "codegemm_gemm", "encode_f16_array", "gemm_group", "gemm_stages", "pack_codes", "phase_split", "random_layer",
     "unpack_codes",
 ]

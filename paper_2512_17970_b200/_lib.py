@@ -41,6 +41,7 @@ EXPORTS = (
     "cg_layer_create",
     "cg_layer_destroy",
     "cg_layer_query",
+    "cg_gemm_stages",
     "cg_layer_gemm",
     "cg_layer_gemm_host",
     "cg_gemm_group",
@@ -113,6 +114,10 @@ def load() -> ctypes.CDLL:
     lib.cg_gemm_group.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp), i,
                                   i, vp]
     lib.cg_gemm_group.restype = i
+    lib.cg_gemm_stages.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                   ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp),
+                                   ctypes.POINTER(ctypes.c_int), i, i, vp]
+    lib.cg_gemm_stages.restype = i
     lib.cg_layer_gemm_host.argtypes = [vp, p, i, p, i, vp]
     lib.cg_layer_gemm_host.restype = i
     lib.cg_layer_psumbook.argtypes = [vp, p, i, p, vp]

@@ -176,7 +176,7 @@ struct cg_layer {
     uint16_t* books = nullptr;      // (m, 2**b, v) binary16
     float* ws = nullptr;            // split-K workspace (n_slices, rows, ws_cols)
     unsigned long long* tickets = nullptr;  // split-K tickets (n_rg, ws_cols), monotonic
-    unsigned long long* zero_ticket = nullptr;  // grid ticket of launches led by this layer
+    unsigned long long* grid_flags = nullptr;  // per-CTA barrier flags of launches led by this layer
     int ws_cols = 0;
     int reserved = 1024;            // driver-reserved smem at the start of the CTA window
     uint16_t* x_dev = nullptr;      // staging for the host entry point
@@ -214,7 +214,7 @@ void free_layer(cg_layer* L) {
     cudaFree(L->books);
     cudaFree(L->ws);
     cudaFree(L->tickets);
-    cudaFree(L->zero_ticket);
+    cudaFree(L->grid_flags);
     cudaFree(L->stamps);
     cudaFree(L->x_dev);
     cudaFree(L->y_dev);
@@ -282,9 +282,11 @@ cg::LayerTask task_of(const cg_layer* L, const uint16_t* x, float* y) {
     return t;
 }
 
-// One launch of the fused kernel for `count` layers (all fast, same v/m/u/kbits/device).
-int launch_same_u(cg_layer* const* layers, const uint16_t* const* xs, float* const* ys, int count,
-                 int n, cudaStream_t s) {
+// One launch of the fused kernel for `count` layers (all fast, same v/m/kbits/device),
+// stages[i] = dependency stage of layer i (non-decreasing; NULL = all stage 0).
+int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const* ys,
+                  const int* stages, int count, int n, cudaStream_t s,
+                  const int* x_dtypes = nullptr) {
     if (count < 1 || count > cg::kMaxGroup)
         return fail(CG_ERR_ARG, "group size %d outside 1..%d", count, cg::kMaxGroup);
     const cg::Plan& p0 = layers[0]->plan;
@@ -295,17 +297,31 @@ int launch_same_u(cg_layer* const* layers, const uint16_t* const* xs, float* con
     gp.pf_dist = layers[0]->pf_dist;
     gp.stamps = layers[0]->stamps;
     cg::FusedSizes zmax{0, 0, 0};
-    int scl_max = 0, rg_max = 0, grid = 1;
+    int scl_max = 0, rg_max = 0, grid = 1, raw_bytes = 0, books_raw = 0;
+    bool x_copy = (n == 1) && !std::getenv("CG_X_REGS");
+    int prev_stage = 0;
     for (int i = 0; i < count; ++i) {
         cg_layer* L = layers[i];
         const cg::Plan& p = L->plan;
         if (!p.fast) return fail(CG_ERR_UNSUPPORTED, "layer %d has no fused kernel", i);
         if (p.v != p0.v || p.m != p0.m || p.kbits != p0.kbits || p.u != p0.u ||
             L->device != layers[0]->device)
-            return fail(CG_ERR_CONFIG, "group layers must share v, m, code width and device");
+            return fail(CG_ERR_CONFIG, "staged launch layers must share v, m, u, code width and device");
+        const int st = stages ? stages[i] : 0;
+        if (st < prev_stage || st > prev_stage + 1 || (i == 0 && st != 0))
+            return fail(CG_ERR_ARG, "stages must start at 0 and grow by at most 1 (layer %d: %d)",
+                        i, st);
+        prev_stage = st;
         int rc = ensure_ws(L, n);
         if (rc) return rc;
         gp.layer[i] = task_of(L, xs[i], ys[i]);
+        gp.layer[i].stage = st;
+        if (x_dtypes && x_dtypes[i] == CG_X_F32) {
+            gp.layer[i].x = nullptr;
+            gp.layer[i].x32 = reinterpret_cast<const float*>(xs[i]);
+        } else if (x_dtypes && x_dtypes[i] != CG_X_F16) {
+            return fail(CG_ERR_ARG, "x_dtypes[%d] = %d is not CG_X_F16 / CG_X_F32", i, x_dtypes[i]);
+        }
         cg::FusedSizes z;
         cg::fused_sizes(p.v, p.m, p.u, p.kbits, &z);
         zmax.psum = std::max(zmax.psum, z.psum);
@@ -314,25 +330,22 @@ int launch_same_u(cg_layer* const* layers, const uint16_t* const* xs, float* con
         scl_max = std::max(scl_max, p.rg_per_task * p.n_gs * 32);
         rg_max = std::max(rg_max, p.rg_per_task);
         grid = std::max(grid, gp.layer[i].n_tasks);
-    }
-    // persistent grid (one wave); if a layer has more tasks than CTAs, the CTA
-    // runs several tasks of it and split-K falls back to last-arriver sums
-    bool multi = grid > layers[0]->sms;
-    grid = std::min(grid, layers[0]->sms);
-    if (multi) gp.flags |= cg::kFlagLastArriver;
-    // fix-up list / owned-ticket targets (deterministic) or the staging buffer
-    // of a task's partial rows (reduce-add): the larger of the two
-    const int cap = rg_max * n + 16;
-    const int list_bytes = (int)list_bytes_for(rg_max, n);
-    int raw_bytes = 0, books_raw = 0;
-    bool x_copy = (n == 1);
-    for (int i = 0; i < count; ++i) {
-        const cg::Plan& p = layers[i]->plan;
         raw_bytes = std::max(raw_bytes, raw_input_bytes(p, p.u));
         books_raw = std::max(books_raw, raw_books_bytes(p));
         // x travels by bulk copy only if every slice of it is a 16-byte multiple
         if ((reinterpret_cast<uintptr_t>(xs[i]) & 15) || (p.cols % 8)) x_copy = false;
     }
+    gp.n_stages = prev_stage + 1;
+    // persistent grid: one CTA per SM, always the full grid (the per-CTA grid
+    // barrier flags rely on every launch making the same arrivals on every
+    // CTA); if a layer has more tasks than CTAs, a CTA runs several tasks of it
+    // and deterministic split-K falls back to last-arriver sums
+    if (grid > layers[0]->sms) gp.flags |= cg::kFlagLastArriver;
+    grid = layers[0]->sms;
+    // fix-up list / owned-ticket targets (deterministic) or the staging buffer
+    // of a task's partial rows (reduce-add): the larger of the two
+    const int cap = rg_max * n + 16;
+    const int list_bytes = (int)list_bytes_for(rg_max, n);
     cg::SmemLayout lay;
     if (!cg::smem_layout(zmax, scl_max, raw_bytes, list_bytes, layers[0]->reserved, &lay,
                          rg_max * 16 * n * 4))
@@ -352,11 +365,11 @@ int launch_same_u(cg_layer* const* layers, const uint16_t* const* xs, float* con
     gp.off_stage[0] = lay.off_list;
     gp.off_stage[1] = lay.off_stage1;
     gp.list_cap = cap;
-    gp.zero_ticket = layers[0]->zero_ticket;
+    gp.grid_flags = layers[0]->grid_flags;
     if (!x_copy) gp.flags |= cg::kFlagXRegs;
     if (layers[0]->flags & CG_OPT_DETERMINISTIC) gp.flags |= cg::kFlagDeterministic;
     if (const char* e = std::getenv("CG_DEBUG_FLAGS")) gp.flags |= std::atoi(e);
-    const bool pdl = !(layers[0]->flags & CG_OPT_NO_PDL);
+    const bool pdl = !(layers[0]->flags & CG_OPT_NO_PDL) && !(gp.flags & cg::kFlagDbgNoPdl);
     CG_CUDA(cg::launch_group_gemv(p0.v, p0.m, p0.u, p0.kbits, gp, grid, lay.total, pdl, s),
             "fused gemv launch");
     return CG_OK;
@@ -381,7 +394,7 @@ int launch_group(cg_layer* const* layers, const uint16_t* const* xs, float* cons
             ++k;
             done[j] = true;
         }
-        int rc = launch_same_u(part, px, py, k, n, s);
+        int rc = launch_stages(part, px, py, nullptr, k, n, s);
         if (rc) return rc;
     }
     return CG_OK;
@@ -547,8 +560,9 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
         if ((rc = ensure_ws(L, 1))) return bail(rc);
     }
     if (p.fast) {
-        if ((rc = dev_alloc(L, &L->zero_ticket, 16, "grid ticket"))) return bail(rc);
-        cudaMemset(L->zero_ticket, 0, 16);
+        const size_t fb = (size_t)(16 + L->sms) * sizeof(unsigned long long);
+        if ((rc = dev_alloc(L, &L->grid_flags, fb, "grid barrier flags"))) return bail(rc);
+        cudaMemset(L->grid_flags, 0, fb);
     }
     if (p.fast && std::getenv("CG_STAMPS")) {
         if ((rc = dev_alloc(L, &L->stamps, (size_t)L->sms * 256, "stamps"))) return bail(rc);
@@ -606,6 +620,19 @@ int cg_gemm_group(cg_layer* const* layers, const void* const* xs, float* const* 
     DeviceGuard guard(layers[0]->device);
     return launch_group(layers, reinterpret_cast<const uint16_t* const*>(xs), ys, count, n,
                         static_cast<cudaStream_t>(stream));
+}
+
+int cg_gemm_stages(cg_layer* const* layers, const void* const* xs, const int* x_dtypes,
+                   float* const* ys, const int* stages, int count, int n, void* stream) {
+    if (!layers || !xs || !ys || !stages) return fail(CG_ERR_ARG, "NULL layers/xs/ys/stages");
+    if (count < 1 || count > cg::kMaxGroup)
+        return fail(CG_ERR_ARG, "launch size %d outside 1..%d", count, cg::kMaxGroup);
+    if (n < 1) return fail(CG_ERR_SHAPE, "x must have >= 1 column, got %d", n);
+    for (int i = 0; i < count; ++i)
+        if (!layers[i] || !xs[i] || !ys[i]) return fail(CG_ERR_ARG, "NULL entry %d", i);
+    DeviceGuard guard(layers[0]->device);
+    return launch_stages(layers, reinterpret_cast<const uint16_t* const*>(xs), ys, stages, count,
+                         n, static_cast<cudaStream_t>(stream), x_dtypes);
 }
 
 int cg_layer_gemm_host(cg_layer* L, const uint16_t* x, int n, float* y, int mode, void* stream) {

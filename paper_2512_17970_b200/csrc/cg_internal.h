@@ -32,20 +32,25 @@ struct LayerTask {
     const uint16_t* scl;      // prepacked scale tiles (binary16 bits)
     const uint16_t* books;    // (m, kcount, v) binary16 bits
     const uint16_t* x;        // (cols, n) binary16 bits
+    const float* x32;         // or (cols, n) binary32, rounded to binary16 when staged
     float* y;                 // (rows, n) output
     float* ws;                // split-K partials (n_slices, rows, n) when n_slices > 1
     unsigned long long* tickets;  // (n_rg, n) monotonic split-K tickets
     int64_t rows, cols, n_rg, n_slices, n_rb;
     int u, rg_per_task, lg, n_gs, kcount, n_tasks;
+    int stage;                // dependency stage within the launch (non-decreasing)
 };
 
-constexpr int kMaxGroup = 8;
+constexpr int kMaxGroup = 16;
 
-// A launch: up to kMaxGroup independent layers sharing (v, m, u, table size)
-// and batch width n.  CTA c runs tasks c, c+grid, ... of every layer in order.
+// A launch: up to kMaxGroup layers sharing (v, m, table size) and batch width
+// n, in dependency stages (layers of one stage are independent; a stage may
+// read what earlier stages wrote).  CTA c runs tasks c, c+grid, ... of every
+// layer of a stage in order; grid barriers separate the stages.
 struct GroupParams {
     LayerTask layer[kMaxGroup];
     int n_layers;
+    int n_stages;             // stage s+1 starts after every CTA finished stage s
     int n;                    // batch columns
     int flags, pf_dist;
     // dynamic shared-memory layout (bytes from the dynamic smem start); the
@@ -54,7 +59,7 @@ struct GroupParams {
     int off_scl[2], off_raw[2];  // double-buffered task inputs: scale tiles, raw books | x
     int raw_x_off;            // byte offset of the raw x slice inside a raw buffer
     int off_stage[2];         // split-K staging of a task's partial rows (reduce-add), x2
-    unsigned long long* zero_ticket;  // {count, generation}: every CTA zeroed its share of y
+    unsigned long long* grid_flags;   // per-CTA barrier flags (zero barrier, stage barriers)
     unsigned long long* stamps;  // diagnostics: per-CTA phase timestamps (8 per CTA) or null
 };
 
@@ -72,6 +77,13 @@ constexpr int kFlagNoPrefetch = 2;
 constexpr int kFlagLastArriver = 4;  // a layer has more tasks than the grid: last arriver sums
 constexpr int kFlagDeterministic = 16;  // split-K by tickets + ordered sums (else L2 reduce-add)
 constexpr int kFlagXRegs = 32;  // x staged through registers (unaligned x / odd cols / n > 1)
+// diagnostics only (CG_DEBUG_FLAGS): wrong results, phase isolation for timing
+constexpr int kFlagDbgSkipBuild = 1 << 8;   // no Psumbook build
+constexpr int kFlagDbgNoLoads = 1 << 9;     // gather reuses the preloaded code tiles
+constexpr int kFlagDbgSkipGather = 1 << 10; // no gather
+constexpr int kFlagDbgEmpty = 1 << 11;      // return at kernel entry
+constexpr int kFlagDbgNoCoop = 1 << 12;     // launch without the cooperative attribute
+constexpr int kFlagDbgNoPdl = 1 << 13;      // launch without programmatic dependent launch
 
 // shared-memory pieces of the fused kernel for (v, m, u, kbits)
 struct FusedSizes {

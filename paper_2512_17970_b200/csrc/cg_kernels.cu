@@ -185,17 +185,21 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed,
 // bank whatever the code (conflict-free lookups).
 //
 // Build: thread (q = lane&7, csub = lane>>3) of warp w writes the entries of
-// lanes 4q..4q+3 (4 segments) for codes csub + 4w + 64i with one STS.128
-// (8 threads of a phase cover one 128-byte code row: conflict-free).  The 4
-// dot products run as 2 FFMA2 chains over k, operands pre-paired:
-//   books2[t][c][k] = (c_k, c_k)   (duplicated binary32 centroid, smem)
-//   x pairs         = (x_{seg0,k}, x_{seg1,k})
+// lanes 4q..4q+3 (4 segments) for codes c0 + 64i, c0 = csub + 4w, with one
+// STS.128 per code (the 8 threads of a phase cover one 128-byte code row:
+// conflict-free).  The 4 dot products run as 2 FFMA2 chains over k:
+//   centroid c_k       binary32 scalar, broadcast to both FFMA2 lanes
+//   x pairs            (x_{seg0,k}, x_{seg1,k}), (x_{seg2,k}, x_{seg3,k})
 // Each entry = ((+0 + c0*x0) + c1*x1) + ...: every lane of an FFMA2 is an
-// IEEE fma with an exact product, i.e. the reference's separate multiply and
-// add (engines.py:126-133), bit for bit.
+// IEEE fma with an exact product (binary16 x binary16 fits binary32), i.e.
+// the reference's separate multiply and add (engines.py:126-133), bit for bit.
 //
-// x is staged transposed and skewed, x32[k][s + s/(4U)], so the 8 threads of
-// a phase (segments 4qU + ...) read 8 different banks.
+// The centroids of a thread's codes are read once per codebook straight from
+// the raw binary16 codebook buffer (TMA-staged) and kept in registers across
+// the U sub-tables; x is staged once per task as binary16 pairs in the layout
+// the FFMA2 operands want (x16_word), 16-byte skewed per lane quad so the 8
+// threads of a phase read 8 distinct bank quads.  Shared-memory traffic of a
+// build is then dominated by the table stores themselves.
 // ---------------------------------------------------------------------------
 template <int V, int M, int U, int KB>
 struct FusedShape {
@@ -204,58 +208,39 @@ struct FusedShape {
     static constexpr int kCodes = 1 << KB;
     static constexpr int kRegionFloats = kCodes * 64;
     static constexpr int kPsumFloats = kRegions * kRegionFloats;
-    static constexpr int kBookFloats = M * kCodes * V * 2;          // duplicated pairs
     static constexpr int kSliceSegs = 32 * U;
-    // x staged pre-paired for FFMA2 (see x_pair_index): per u, per lane quad q,
-    // 2V float2 pairs, plus a 16-byte skew per q (conflict-free 128-bit loads)
-    static constexpr int kXQuad = 4 * V + 4;  // floats per (u, q) incl. skew pad
-    static constexpr int kXFloats = U * 8 * kXQuad;
+    // staged x: per (u, lane quad q) a block of 2V binary16 pairs + skew
+    static constexpr int kXQW = V <= 4 ? 12 : 2 * V + 4;  // 32-bit words per block
+    static constexpr int kXWords = U * 8 * kXQW;
     static constexpr int kPsumBytes = 4 * kPsumFloats;
-    static constexpr int kBookBytes = 4 * kBookFloats;
-    static constexpr int kXBytes = 4 * kXFloats;
+    static constexpr int kXBytes = 4 * kXWords;
     static constexpr int kTileBytes = M * U * 512;  // codes per (slice, row group)
-    static constexpr int kBookPerThread = (M * kCodes * V + kThreads - 1) / kThreads;
     static constexpr int kXPerThread = (V * kSliceSegs + kThreads - 1) / kThreads;
+    static constexpr int kCPT = kCodes / (4 * kWarps) > 0 ? kCodes / (4 * kWarps) : 1;
+    static constexpr bool kFullCodes = kCPT * 4 * kWarps == kCodes;
+    // centroids of all of a thread's codes held in registers across u
+    #ifdef CG_NOHOIST
+    static constexpr bool kHoist = false;
+#else
+    static constexpr bool kHoist = kCPT * V <= 32;
+#endif
+    // register pipeline depth of the code-tile stream (tiles of 16*M*U bytes per lane)
+    #ifdef CG_DEPTH
+    static constexpr int kDepth = CG_DEPTH;
+#else
+    static constexpr int kDepth = M * U < 4 ? 3 : 2;
+#endif
 };
 
-// Element k of slice segment s lives in the pair (x_{s0,k}, x_{s1,k}) with
-// s0,s1 = segments of lanes 4q+2h, 4q+2h+1 at the same u: the build thread of
-// quad q loads its 2V pairs with V 128-bit loads into aligned register pairs.
+// binary16 index (in the staged x buffer) of element k of slice segment s:
+// the pair (x_{s0,k}, x_{s1,k}) of lanes 4q+2h, 4q+2h+1 at the same u is one
+// 32-bit word, half lo.
 template <int V, int M, int U, int KB>
-__device__ __forceinline__ int x_pair_index(int s, int k) {
+__device__ __forceinline__ int x16_index(int s, int k) {
     using S = FusedShape<V, M, U, KB>;
     const int l = s / U, u = s - (s / U) * U;
     const int q = l >> 2, i = l & 3, h = i >> 1, lo = i & 1;
-    return (u * 8 + q) * S::kXQuad + ((h * V + k) << 1) + lo;
-}
-
-// Load this thread's share of the codebooks (binary16) into registers.
-template <int V, int M, int U, int KB>
-__device__ __forceinline__ void load_books(uint16_t (&r)[FusedShape<V, M, U, KB>::kBookPerThread],
-                                           const uint16_t* books, int kcount, int tid) {
-    using S = FusedShape<V, M, U, KB>;
-#pragma unroll
-    for (int i = 0; i < S::kBookPerThread; ++i) {
-        const int e = tid + i * kThreads;
-        r[i] = e < M * kcount * V ? books[e] : (uint16_t)0;
-    }
-}
-
-template <int V, int M, int U, int KB>
-__device__ __forceinline__ void store_books(
-    float2* books2, const uint16_t (&r)[FusedShape<V, M, U, KB>::kBookPerThread], int kcount,
-    int tid) {
-    using S = FusedShape<V, M, U, KB>;
-#pragma unroll
-    for (int i = 0; i < S::kBookPerThread; ++i) {
-        const int e = tid + i * kThreads;
-        if (e < M * kcount * V) {
-            const int t = e / (kcount * V);
-            const int rest = e - t * kcount * V;  // c*V + k
-            const float f = h2f(r[i]);
-            books2[t * S::kCodes * V + rest] = make_float2(f, f);
-        }
-    }
+    return (((u * 8 + q) * S::kXQW + h * V + k) << 1) | lo;
 }
 
 // Load this thread's share of the slice of x (column `col`), binary16.
@@ -273,87 +258,149 @@ __device__ __forceinline__ void load_x(uint16_t (&r)[FusedShape<V, M, U, KB>::kX
     }
 }
 
+// A layer's x given as binary32 (an earlier stage's y, written in this
+// launch: read through L2) is rounded to binary16 (RNE) as it is staged.
 template <int V, int M, int U, int KB>
-__device__ __forceinline__ void store_x(float* x32,
+__device__ __forceinline__ void load_x(uint16_t (&r)[FusedShape<V, M, U, KB>::kXPerThread],
+                                       const LayerTask& L, int64_t slice, int n, int col, int tid) {
+    using S = FusedShape<V, M, U, KB>;
+    if (L.x32 == nullptr) return load_x<V, M, U, KB>(r, L.x, slice, L.cols, n, col, tid);
+    const int64_t e0 = slice * (int64_t)(S::kSliceSegs * V);
+#pragma unroll
+    for (int i = 0; i < S::kXPerThread; ++i) {
+        const int l = tid + i * kThreads;
+        const int64_t e = e0 + l;
+        r[i] = (l < S::kSliceSegs * V && e < L.cols)
+                   ? __half_as_ushort(__float2half_rn(__ldcg(L.x32 + e * n + col)))
+                   : (uint16_t)0;
+    }
+}
+
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void store_x(uint16_t* x16,
                                         const uint16_t (&r)[FusedShape<V, M, U, KB>::kXPerThread],
                                         int tid) {
     using S = FusedShape<V, M, U, KB>;
 #pragma unroll
     for (int i = 0; i < S::kXPerThread; ++i) {
         const int l = tid + i * kThreads;
-        if (l < S::kSliceSegs * V) x32[x_pair_index<V, M, U, KB>(l / V, l % V)] = h2f(r[i]);
+        if (l < S::kSliceSegs * V) x16[x16_index<V, M, U, KB>(l / V, l % V)] = r[i];
     }
 }
 
+// raw binary16 x slice (TMA-staged, `valid` elements) -> staged pairs, zero past the end
 template <int V, int M, int U, int KB>
-__device__ __forceinline__ void build_psumbook_smem(float* psum, const float2* books2,
-                                                    const float* x32, int kcount, int tid) {
+__device__ __forceinline__ void stage_x_raw(uint16_t* x16, const uint16_t* xr, int valid, int tid) {
+    using S = FusedShape<V, M, U, KB>;
+    for (int e = tid; e < S::kSliceSegs * V; e += kThreads)
+        x16[x16_index<V, M, U, KB>(e / V, e % V)] = e < valid ? xr[e] : (uint16_t)0;
+}
+
+// V binary16 centroid components -> binary32
+template <int V>
+__device__ __forceinline__ void load_centroid(float (&c)[V], const uint16_t* p) {
+    uint32_t w[V / 2 > 0 ? V / 2 : 1];
+    if constexpr (V == 2) {
+        w[0] = *reinterpret_cast<const uint32_t*>(p);
+    } else if constexpr (V == 4) {
+        const uint2 a = *reinterpret_cast<const uint2*>(p);
+        w[0] = a.x;
+        w[1] = a.y;
+    } else {
+#pragma unroll
+        for (int i = 0; i < V / 8; ++i) {
+            const uint4 a = reinterpret_cast<const uint4*>(p)[i];
+            w[4 * i] = a.x;
+            w[4 * i + 1] = a.y;
+            w[4 * i + 2] = a.z;
+            w[4 * i + 3] = a.w;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < V / 2; ++i) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+        c[2 * i] = f.x;
+        c[2 * i + 1] = f.y;
+    }
+}
+
+// entries of codes c (4 lanes 4q..4q+3) for one sub-table: 2 FFMA2 chains
+template <int V>
+__device__ __forceinline__ void psum_entries(float* dst, const float (&cc)[V],
+                                             const float2 (&x01)[V], const float2 (&x23)[V]) {
+    float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        a01 = __ffma2_rn(make_float2(cc[k], cc[k]), x01[k], a01);
+        a23 = __ffma2_rn(make_float2(cc[k], cc[k]), x23[k], a23);
+    }
+    *reinterpret_cast<float4*>(dst) = make_float4(a01.x, a01.y, a23.x, a23.y);
+}
+
+// books16: raw binary16 codebooks [t][kcount][V];  x16: staged x pairs
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void build_psumbook_smem(float* psum, const uint16_t* books16,
+                                                    const uint32_t* x16w, int kcount, int tid) {
     using S = FusedShape<V, M, U, KB>;
     const int lane = tid & 31, warp = tid >> 5;
-    const int q = lane & 7;     // this thread writes lanes 4q..4q+3 of a code row
-    const int csub = lane >> 3; // 4 codes per warp per pass
-    // codes this thread owns: c0 + 64*i; all of them in flight at once when the
-    // table is full size (kcount == 2**KB): 2*CPT independent FFMA2 chains
-    constexpr int kCPT = S::kCodes / (4 * kWarps) > 0 ? S::kCodes / (4 * kWarps) : 1;
+    const int q = lane & 7;      // this thread writes lanes 4q..4q+3 of a code row
+    const int csub = lane >> 3;  // 4 codes per warp per pass
     const int c0 = csub + 4 * warp;
+    constexpr int kCPT = S::kCPT;
+    const bool full = S::kFullCodes && kcount == S::kCodes;
 #pragma unroll 1
-    for (int j = 0; j < S::kSub; ++j) {
-        const int t = j / U, uu = j % U;
-        // x of this thread's 4 segments, already paired for FFMA2:
-        // x01[k] = (x_s0k, x_s1k), x23[k] = (x_s2k, x_s3k)
-        float2 x01[V], x23[V];
-        {
-            const float4* src = reinterpret_cast<const float4*>(x32 + (uu * 8 + q) * S::kXQuad);
+    for (int t = 0; t < M; ++t) {
+        const uint16_t* bk = books16 + t * kcount * V;
+        float cc[S::kHoist ? kCPT : 1][V];
+        if constexpr (S::kHoist) {
 #pragma unroll
-            for (int c = 0; c < V; ++c) {  // 2V pairs = V float4
-                const float4 w = src[c];
-                float2* dstp = (2 * c < V) ? &x01[2 * c] : &x23[2 * c - V];
-                dstp[0] = make_float2(w.x, w.y);
-                dstp[1] = make_float2(w.z, w.w);
+            for (int i = 0; i < kCPT; ++i) {
+                const int c = c0 + 4 * kWarps * i;
+                if (full || c < kcount) load_centroid<V>(cc[i], bk + c * V);
             }
         }
-        float* dst = psum + (j >> 1) * S::kRegionFloats + (j & 1) * 32 + q * 4;
-        const float2* bk = books2 + t * S::kCodes * V;
-        if (kcount == S::kCodes && kCPT * 4 * kWarps == S::kCodes) {
-            float2 cc[kCPT][V];
-#pragma unroll
-            for (int i = 0; i < kCPT; ++i) {
-                const float4* src = reinterpret_cast<const float4*>(bk + (c0 + 4 * kWarps * i) * V);
-#pragma unroll
-                for (int k = 0; k < V; k += 2) {
-                    const float4 w = src[k / 2];
-                    cc[i][k] = make_float2(w.x, w.y);
-                    if (k + 1 < V) cc[i][k + 1] = make_float2(w.z, w.w);
-                }
-            }
-            float2 a01[kCPT], a23[kCPT];
-#pragma unroll
-            for (int i = 0; i < kCPT; ++i) {
-                a01[i] = make_float2(0.0f, 0.0f);
-                a23[i] = make_float2(0.0f, 0.0f);
-            }
-#pragma unroll
-            for (int k = 0; k < V; ++k)
-#pragma unroll
-                for (int i = 0; i < kCPT; ++i) {
-                    a01[i] = __ffma2_rn(cc[i][k], x01[k], a01[i]);
-                    a23[i] = __ffma2_rn(cc[i][k], x23[k], a23[i]);
-                }
-#pragma unroll
-            for (int i = 0; i < kCPT; ++i)
-                *reinterpret_cast<float4*>(dst + (c0 + 4 * kWarps * i) * 64) =
-                    make_float4(a01[i].x, a01[i].y, a23[i].x, a23[i].y);
-        } else {
 #pragma unroll 1
-            for (int c = c0; c < kcount; c += 4 * kWarps) {
-                float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
+        for (int uu = 0; uu < U; ++uu) {
+            const int j = t * U + uu;
+            // x of this thread's 4 segments, paired for FFMA2:
+            // x01[k] = (x_s0k, x_s1k), x23[k] = (x_s2k, x_s3k)
+            float2 x01[V], x23[V];
+            {
+                const uint32_t* src = x16w + (uu * 8 + q) * S::kXQW;
+                uint32_t w[2 * V];
+#pragma unroll
+                for (int i = 0; i < 2 * V; i += 4) {
+                    if (i + 4 <= 2 * V) {
+                        const uint4 a = *reinterpret_cast<const uint4*>(src + i);
+                        w[i] = a.x;
+                        w[i + 1] = a.y;
+                        w[i + 2] = a.z;
+                        w[i + 3] = a.w;
+                    } else {  // V == 1 never instantiated; 2V == 4 covers V == 2
+                        w[i] = src[i];
+                        w[i + 1] = src[i + 1];
+                    }
+                }
 #pragma unroll
                 for (int k = 0; k < V; ++k) {
-                    const float2 cc = bk[c * V + k];
-                    a01 = __ffma2_rn(cc, x01[k], a01);
-                    a23 = __ffma2_rn(cc, x23[k], a23);
+                    x01[k] = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+                    x23[k] = __half22float2(*reinterpret_cast<const __half2*>(&w[V + k]));
                 }
-                *reinterpret_cast<float4*>(dst + c * 64) = make_float4(a01.x, a01.y, a23.x, a23.y);
+            }
+            float* dst = psum + (j >> 1) * S::kRegionFloats + (j & 1) * 32 + q * 4;
+            if constexpr (S::kHoist) {
+#pragma unroll
+                for (int i = 0; i < kCPT; ++i) {
+                    const int c = c0 + 4 * kWarps * i;
+                    if (full || c < kcount) psum_entries<V>(dst + c * 64, cc[i], x01, x23);
+                }
+            } else {
+#pragma unroll 1
+                for (int c = c0; c < kcount; c += 4 * kWarps) {
+                    float ci[V];
+                    load_centroid<V>(ci, bk + c * V);
+                    psum_entries<V>(dst + c * 64, ci, x01, x23);
+                }
             }
         }
     }
@@ -554,21 +601,14 @@ __device__ __forceinline__ float sum_slices(const LayerTask& L, int n, int64_t r
     const int ns = (int)L.n_slices;
     const int64_t plane = L.rows * n;
     const float* src = L.ws + row * n + col;
-    float acc = 0.0f;
-    for (int s0 = 0; s0 < ns; s0 += 16) {
-        float v[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (s0 + k < ns) v[k] = __ldcg(src + (int64_t)(s0 + k) * plane);
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (s0 + k < ns) acc = (s0 + k == 0) ? v[k] : acc + v[k];
-    }
+    float acc = __ldcg(src);
+#pragma unroll 4
+    for (int s = 1; s < ns; ++s) acc += __ldcg(src + (int64_t)s * plane);
     return acc;
 }
 
 // whole row group (16 rows) by lanes 0-15 of a warp
-__device__ __noinline__ void fixup_row_group(const LayerTask& L, int n, int64_t rg, int col,
+__device__ __forceinline__ void fixup_row_group(const LayerTask& L, int n, int64_t rg, int col,
                                              int lane) {
     const int64_t row = rg * 16 + lane;
     if (lane < 16 && row < L.rows) L.y[row * n + col] = sum_slices(L, n, row, col);
@@ -587,15 +627,42 @@ struct CtaState {
     uint64_t in_bar[2];           // mbarriers of the two task-input buffers
     int list_count;
     unsigned in_phase;            // parity bit per input buffer
-    unsigned long long zero_gen;  // grid generation seen at arrival
+    unsigned long long bar_base;  // this CTA's grid flag at launch start
+    int n_arrive;                 // grid-barrier arrivals so far in this launch
     int zero_ready;
     int prev_layer;
     long long prev_slice, prev_rg0, prev_rg1;
+    int n_bar;                    // stage barriers passed (diagnostics)
 };
 struct PrevTask {
     int layer;
     long long slice, rg0, rg1;
 };
+
+// ---- grid barriers: one monotonic arrival counter ----
+// grid_flags[0] counts barrier arrivals of all CTAs over all launches that used
+// this array; grid_flags[16 + c] (another cache line) is CTA c's own arrival
+// count, read at launch start.  Every such launch runs the full grid and every
+// CTA makes the same arrivals, so at launch start counter = grid * own.
+// Arrival k is a release reduction (fire-and-forget, no contended round trip);
+// waiting for arrival k polls the counter until it reaches grid * (own + k).
+__device__ __forceinline__ void grid_arrive(const GroupParams& p, CtaState& cs) {
+    ++cs.n_arrive;
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(p.grid_flags) : "memory");
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.grid_flags + 16 + blockIdx.x),
+                 "l"(cs.bar_base + (unsigned long long)cs.n_arrive)
+                 : "memory");
+}
+// one thread; returns once every CTA made arrival k
+__device__ __forceinline__ void grid_wait(const GroupParams& p, const CtaState& cs, int k) {
+    const unsigned long long want = (cs.bar_base + (unsigned long long)k) * gridDim.x;
+    unsigned long long f;
+    while (true) {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(p.grid_flags) : "memory");
+        if (f >= want) break;
+        __nanosleep(32);
+    }
+}
 
 // Split-K close of a task.  Every (row group, column) of the task takes a
 // ticket (acq_rel atomic: releases our partials, acquires the others').
@@ -684,48 +751,69 @@ __device__ __forceinline__ bool next_task(const GroupParams& p, TaskCoord& c) {
     return c.l < p.n_layers;
 }
 
-__device__ __forceinline__ bool x_by_copy(const GroupParams& p) {
-    return p.n == 1 && !(p.flags & kFlagXRegs);
+__device__ __forceinline__ bool x_by_copy(const GroupParams& p, const LayerTask& L) {
+    return p.n == 1 && !(p.flags & kFlagXRegs) && L.x32 == nullptr;
 }
 
-// tid 0 only.  weights: scale tiles + codebooks; x: the slice of x (n == 1).
+// Task geometry (all task counts fit in 32 bits).
+struct TaskGeom {
+    int slice, rb;
+    int64_t rg0, rg1;
+};
+__device__ __forceinline__ TaskGeom task_geom(const LayerTask& L, int64_t t) {
+    TaskGeom g;
+    g.slice = (int)t / (int)L.n_rb;
+    g.rb = (int)t - g.slice * (int)L.n_rb;
+    g.rg0 = (int64_t)g.rb * L.rg_per_task;
+    g.rg1 = min(g.rg0 + (int64_t)L.rg_per_task, L.n_rg);
+    return g;
+}
+
+// One thread.  weights: scale tiles + codebooks (TMA bulk -> smem, mbarrier)
+// and, unless disabled, a bulk L2 prefetch of the task's whole code range
+// (contiguous in the prepacked layout) so HBM streams the codes while the
+// CTA waits for x and builds the table; x: the slice of x (n == 1).
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ void issue_inputs(const GroupParams& p, TaskCoord c, int buf,
                                              unsigned char* smem_raw, bool weights, bool x) {
     using S = FusedShape<V, M, U, KB>;
     const LayerTask& L = p.layer[c.l];
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
-    const int64_t slice = (int)c.t / (int)L.n_rb;
-    const int64_t rb = (int)c.t - (int)slice * (int)L.n_rb;
-    const int64_t rg0 = rb * L.rg_per_task;
-    const int64_t rg1 = min(rg0 + (int64_t)L.rg_per_task, L.n_rg);
-    const uint32_t scl_bytes = (uint32_t)((rg1 - rg0) * L.n_gs * 32);
+    const TaskGeom g = task_geom(L, c.t);
+    const uint32_t scl_bytes = (uint32_t)((g.rg1 - g.rg0) * L.n_gs * 32);
     const uint32_t book_bytes = (uint32_t)((M * L.kcount * V * 2 + 15) & ~15);  // alloc is padded
-    const int64_t e0 = slice * (int64_t)(S::kSliceSegs * V);
+    const int64_t e0 = (int64_t)g.slice * (S::kSliceSegs * V);
     const int64_t xn = min((int64_t)(S::kSliceSegs * V), L.cols - e0);
-    const uint32_t x_bytes = x_by_copy(p) ? (uint32_t)(xn * 2) : 0u;  // host: 16-B multiple
+    const uint32_t x_bytes = x_by_copy(p, L) ? (uint32_t)(xn * 2) : 0u;  // host: 16-B multiple
     uint64_t* bar = &cs.in_bar[buf];
     unsigned char* raw = smem_raw + p.off_raw[buf];
     if (weights) {
         mbar_expect_tx(bar, scl_bytes + book_bytes + x_bytes);
-        bulk_g2s(smem_raw + p.off_scl[buf], L.scl + (slice * L.n_rg + rg0) * L.n_gs * 16,
+        bulk_g2s(smem_raw + p.off_scl[buf], L.scl + ((int64_t)g.slice * L.n_rg + g.rg0) * L.n_gs * 16,
                  scl_bytes, bar);
         bulk_g2s(raw, L.books, book_bytes, bar);
+        if (!(p.flags & kFlagNoPrefetch)) {
+            const uint8_t* base =
+                L.codes + ((int64_t)g.slice * L.n_rg + g.rg0) * (int64_t)S::kTileBytes;
+            const int64_t bytes = (g.rg1 - g.rg0) * (int64_t)S::kTileBytes;
+            constexpr int64_t kChunk = 32 * 1024;
+            for (int64_t o = 0; o < bytes; o += kChunk)
+                prefetch_l2_bulk(base + o, (uint32_t)min(kChunk, bytes - o));
+        }
     }
     if (x && x_bytes) bulk_g2s(raw + p.raw_x_off, L.x + e0, x_bytes, bar);
 }
 
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int buf, bool first_task,
-                                         bool has_next, TaskCoord nc, unsigned char* smem_raw,
-                                         int tid, int task_idx) {
+                                         bool has_next, bool x_next, TaskCoord nc,
+                                         unsigned char* smem_raw, int tid, int task_idx) {
     using S = FusedShape<V, M, U, KB>;
+    constexpr int D = S::kDepth;
     const int l = c.l;
-    const int64_t task = c.t;
     const LayerTask& L = p.layer[l];
     float* psum = reinterpret_cast<float*>(smem_raw + p.off_psum);
-    float2* books2 = reinterpret_cast<float2*>(smem_raw + p.off_books);
-    float* x32 = reinterpret_cast<float*>(smem_raw + p.off_x);
+    uint16_t* x16 = reinterpret_cast<uint16_t*>(smem_raw + p.off_x);
     const uint16_t* scl_s = reinterpret_cast<const uint16_t*>(smem_raw + p.off_scl[buf]);
     const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem_raw + p.off_raw[buf]);
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
@@ -736,54 +824,37 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
 
     const int lane = tid & 31, warp = tid >> 5;
     const int n = p.n;
-    const int slice = (int)task / (int)L.n_rb;  // task counts fit in 32 bits
-    const int rb = (int)task - slice * (int)L.n_rb;
-    const int64_t rg0 = (int64_t)rb * L.rg_per_task;
-    const int64_t rg1 = min(rg0 + (int64_t)L.rg_per_task, L.n_rg);
+    const TaskGeom g = task_geom(L, c.t);
+    const int slice = g.slice;
+    const int64_t rg0 = g.rg0, rg1 = g.rg1;
     const int n_gs = L.n_gs;
     const uint8_t* tiles = L.codes + (int64_t)slice * L.n_rg * (int64_t)S::kTileBytes;
     const bool split = L.n_slices > 1;
     CG_STAMP(0)
 
-    // 1. this task's first code tiles towards L2 (codebooks, x and scales were
-    //    put in flight one task earlier, or before griddepcontrol.wait)
+    // 1. this warp's first D code tiles into registers: they travel (from L2,
+    //    where the task's range was bulk-prefetched) during the input wait
+    //    and the table build
     const int my_rgs = rg0 + warp < rg1 ? (int)((rg1 - rg0 - warp + kWarps - 1) / kWarps) : 0;
     const uint8_t* cptr = tiles + (rg0 + warp) * S::kTileBytes + lane * 16;
     constexpr int64_t kStep = (int64_t)kWarps * S::kTileBytes;
-    const uint8_t* wtile = tiles + (rg0 + warp) * S::kTileBytes;
-    const int pf = (p.flags & kFlagNoPrefetch) ? 0 : p.pf_dist;
-    if (!(p.flags & kFlagNoPrefetch) && lane < 2 + pf && lane < my_rgs)
-        prefetch_l2_bulk(wtile + lane * kStep, S::kTileBytes);
+    uint4 tb[D][M][U];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+        if (d < my_rgs) load_tile<V, M, U, KB>(tb[d], cptr + d * kStep);
     uint16_t xreg[S::kXPerThread];
-    if (!x_by_copy(p)) load_x<V, M, U, KB>(xreg, L.x, slice, L.cols, n, 0, tid);
+    if (!x_by_copy(p, L)) load_x<V, M, U, KB>(xreg, L, slice, n, 0, tid);
 
     // 2. the previous task is done with the table; the staging buffer of two
-    //    tasks ago has been read by its flush; close the previous task's row
-    //    groups (deterministic mode); the next task's inputs start travelling
+    //    tasks ago has been read by its flush; the next task's inputs start
+    //    travelling; close the previous task's row groups (deterministic mode)
     if (tid == 0) bulk_wait_read_prev();
     __syncthreads();
     CG_STAMP(7)
-    if (tid == kThreads - 32 && has_next)
-        issue_inputs<V, M, U, KB>(p, nc, buf ^ 1, smem_raw, true, true);
+    if (tid == kThreads - 32 && has_next) issue_inputs<V, M, U, KB>(p, nc, buf ^ 1, smem_raw, true, x_next);
     close_task(p, smem_raw, tid);
     mbar_wait(&cs.in_bar[buf], (cs.in_phase >> buf) & 1u);
     CG_STAMP(4)
-    // raw binary16 codebooks -> duplicated binary32 pairs
-    if (L.kcount == S::kCodes) {  // full-size tables: same index, two halves per thread
-        const uint32_t* raw2 = reinterpret_cast<const uint32_t*>(raw);
-        float4* b4 = reinterpret_cast<float4*>(books2);
-        for (int e = tid; e < M * S::kCodes * V / 2; e += kThreads) {
-            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&raw2[e]));
-            b4[e] = make_float4(f.x, f.x, f.y, f.y);
-        }
-    } else {
-        for (int e = tid; e < M * L.kcount * V; e += kThreads) {
-            const int t = e / (L.kcount * V);
-            const float f = h2f(raw[e]);
-            books2[t * S::kCodes * V + (e - t * L.kcount * V)] = make_float2(f, f);
-        }
-    }
-    CG_STAMP(1)
 
     // per-lane constants of the gather (Psumbook base must be 64 KB aligned)
     const uint32_t psum_addr = smem_u32(psum);
@@ -797,76 +868,74 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     const int gi = lg >= 5 ? 0 : (lane >> lg);
     const uint16_t* sp0 = scl_s + (warp * n_gs + gi) * 16 + sbase;
     const int sstep = kWarps * n_gs * 16;
-    uint4 bufA[M][U], bufB[M][U];
+    const bool stage_out = split && !(p.flags & kFlagDeterministic);
+    const int64_t row_step = (int64_t)kWarps * 16;
 
     for (int col = 0; col < n; ++col) {
         if (col > 0) {
             __syncthreads();  // previous column's table is no longer read
-            load_x<V, M, U, KB>(xreg, L.x, slice, L.cols, n, col, tid);
+            load_x<V, M, U, KB>(xreg, L, slice, n, col, tid);
         }
-        if (x_by_copy(p)) {
-            // raw binary16 x slice (zero past the layer's last column)
-            const uint16_t* xr = raw + p.raw_x_off / 2;
-            const int64_t e0 = slice * (int64_t)(S::kSliceSegs * V);
-            for (int e = tid; e < S::kSliceSegs * V; e += kThreads)
-                x32[x_pair_index<V, M, U, KB>(e / V, e % V)] =
-                    (e0 + e < L.cols) ? h2f(xr[e]) : 0.0f;
+        if (x_by_copy(p, L)) {
+            const int64_t e0 = (int64_t)slice * (S::kSliceSegs * V);
+            stage_x_raw<V, M, U, KB>(x16, raw + p.raw_x_off / 2,
+                                     (int)min((int64_t)(S::kSliceSegs * V), L.cols - e0), tid);
         } else {
-            store_x<V, M, U, KB>(x32, xreg, tid);
+            store_x<V, M, U, KB>(x16, xreg, tid);
         }
         __syncthreads();
         if (col == 0) CG_STAMP(5)
-        build_psumbook_smem<V, M, U, KB>(psum, books2, x32, L.kcount, tid);
+        if (!(p.flags & kFlagDbgSkipBuild))
+            build_psumbook_smem<V, M, U, KB>(psum, raw, reinterpret_cast<const uint32_t*>(x16),
+                                             L.kcount, tid);
         __syncthreads();
         if (col == 0) CG_STAMP(6)
         if (col == 0 && first_task) pdl_launch_dependents();
-        if (my_rgs > 0) load_tile<V, M, U, KB>(bufA, cptr);
-        if (col == 0) CG_STAMP(2)
-        const bool stage_out = split && !(p.flags & kFlagDeterministic);
+        if (col > 0) {
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+                if (d < my_rgs) load_tile<V, M, U, KB>(tb[d], cptr + d * kStep);
+        }
         float* out = stage_out ? reinterpret_cast<float*>(smem_raw + p.off_stage[buf]) - rg0 * 16 * n
-                               : (split ? L.ws + slice * L.rows * n : L.y);
+                               : (split ? L.ws + (int64_t)slice * L.rows * n : L.y);
         int64_t row = (rg0 + warp) * 16 + mask;
-        const int64_t row_step = (int64_t)kWarps * 16;
-        for (int i = 0; i < my_rgs; i += 2) {
-            if (col == 0 && lane < 2 && i + 1 + pf + lane < my_rgs && pf > 0)
-                prefetch_l2_bulk(wtile + (i + 1 + pf + lane) * kStep, S::kTileBytes);
-            if (i + 1 < my_rgs) load_tile<V, M, U, KB>(bufB, cptr + (i + 1) * kStep);
-            float v = gather_row_group<V, M, U, KB>(bufA, sp0 + i * sstep, lb0, lb1, lg, mask);
-            if (lane < 16 && row < L.rows) out[row * n + col] = v;
-            row += row_step;
-            if (i + 1 < my_rgs) {
-                if (i + 2 < my_rgs) load_tile<V, M, U, KB>(bufA, cptr + (i + 2) * kStep);
-                v = gather_row_group<V, M, U, KB>(bufB, sp0 + (i + 1) * sstep, lb0, lb1, lg, mask);
-                if (lane < 16 && row < L.rows) out[row * n + col] = v;
-                row += row_step;
+        // D-deep register pipeline: tile i+D is requested as soon as tile i is consumed
+        const int n_rgs = (p.flags & kFlagDbgSkipGather) ? 0 : my_rgs;
+        const int load_rgs = (p.flags & kFlagDbgNoLoads) ? 0 : my_rgs;
+        for (int i0 = 0; i0 < n_rgs; i0 += D) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const int i = i0 + d;
+                if (i < n_rgs) {
+                    const float v = gather_row_group<V, M, U, KB>(tb[d], sp0 + i * sstep, lb0, lb1,
+                                                                  lg, mask);
+                    if (i + D < load_rgs) load_tile<V, M, U, KB>(tb[d], cptr + (i + D) * kStep);
+                    if (lane < 16 && row < L.rows) out[row * n + col] = v;
+                    row += row_step;
+                }
             }
         }
     }
-    if (split && !(p.flags & kFlagDeterministic)) {
+    CG_STAMP(1)
+    if (stage_out) {
         // flush the task's partial rows into y (L2 reduce-add); y was zeroed
-        // by the grid at kernel start -- wait for that once
+        // by the grid at kernel start -- wait for that (arrival 1) once
         __syncthreads();
-        if (tid == 0) {
-            if (!cs.zero_ready) {
-                // sense-reversal grid barrier on {count, generation}: wait for
-                // the generation recorded at arrival to move on
-                const unsigned long long g0 = cs.zero_gen;
-                unsigned long long cur;
-                do {
-                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];"
-                                 : "=l"(cur)
-                                 : "l"(p.zero_ticket + 1)
-                                 : "memory");
-                } while (cur == g0);
-                asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (warp == 0) {
+            if (lane == 0) {
+                if (!cs.zero_ready) {
+                    grid_wait(p, cs, 1);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
                 cs.zero_ready = 1;
+                CG_STAMP(2)
+                const float* stage = reinterpret_cast<const float*>(smem_raw + p.off_stage[buf]);
+                const int64_t r1 = min(rg1 * 16, L.rows);
+                const int64_t elems = (r1 - rg0 * 16) * n;
+                const int64_t body = elems & ~int64_t(3);  // 16-byte multiple
+                if (body > 0) bulk_reduce_add_f32(L.y + rg0 * 16 * n, stage, (uint32_t)(body * 4));
+                for (int64_t e = body; e < elems; ++e) atomicAdd(L.y + rg0 * 16 * n + e, stage[e]);
             }
-            const float* stage = reinterpret_cast<const float*>(smem_raw + p.off_stage[buf]);
-            const int64_t r1 = min(rg1 * 16, L.rows);
-            const int64_t elems = (r1 - rg0 * 16) * n;
-            const int64_t body = elems & ~int64_t(3);  // 16-byte multiple
-            if (body > 0) bulk_reduce_add_f32(L.y + rg0 * 16 * n, stage, (uint32_t)(body * 4));
-            for (int64_t e = body; e < elems; ++e) atomicAdd(L.y + rg0 * 16 * n + e, stage[e]);
         }
     }
     __syncthreads();
@@ -881,19 +950,54 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
 #undef CG_STAMP
 }
 
+// Grid barrier between dependent stages of a launch (sense reversal on
+// {count, generation}).  Everything this CTA wrote in the stage -- plain
+// stores and the bulk (async-proxy) reduce-adds -- is complete and released
+// before the arrival; the next stage's x, read by TMA, is acquired after.
+__device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned char* smem_raw,
+                                              int tid) {
+    __syncthreads();
+    close_task(p, smem_raw, tid);  // deterministic split-K: pending ordered sums
+    CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
+    unsigned long long* st = p.stamps ? p.stamps + blockIdx.x * 32 + 24 : nullptr;
+    const bool first_bar = cs.n_bar == 0;  // stamps of the first barrier only
+    if (tid == 0) {
+        if (st && first_bar) st[0] = gtimer();
+        cs.prev_layer = -1;
+        bulk_wait_all();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (st && first_bar) st[1] = gtimer();
+        grid_arrive(p, cs);
+        if (st && first_bar) st[2] = gtimer();
+        grid_wait(p, cs, cs.n_arrive);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (st && first_bar) st[3] = gtimer();
+        ++cs.n_bar;
+    }
+    __syncthreads();
+}
+
+// A launch runs a chain of stages (all layers share the tiling u: one
+// instantiation per (v, m, u, code width)); the layers of one stage are independent
+// (a grouped launch: {q,k,v}, {gate,up}), stage s+1 may read what stage s
+// wrote (its x is stage s's y).  CTA c runs tasks c, c+grid, ... of every
+// layer of a stage, in layer order; stages are separated by grid barriers.
+// The next task's weights (codebooks, scale tiles, code range into L2) are
+// requested one task ahead -- across a stage boundary too -- and its x as
+// soon as it is safe (same stage: at once; next stage: after the barrier).
 template <int V, int M, int U, int KB>
 __global__ void __launch_bounds__(kThreads, 1)
     group_gemv_kernel(const __grid_constant__ GroupParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (p.flags & kFlagDbgEmpty) return;
     const int tid = threadIdx.x;
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
     TaskCoord c{0, (int64_t)blockIdx.x};
-    bool have = true;
     while (c.l < p.n_layers && c.t >= p.layer[c.l].n_tasks) {
         ++c.l;
         c.t = blockIdx.x;
     }
-    have = c.l < p.n_layers;
+    bool have = c.l < p.n_layers;
     if (tid == 0) {
         mbar_init(&cs.in_bar[0], 1);
         mbar_init(&cs.in_bar[1], 1);
@@ -901,12 +1005,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         cs.in_phase = 0;
         cs.zero_ready = 0;
         cs.prev_layer = -1;
-        // weights of the first task travel before the wait on the previous kernel
+        cs.n_bar = 0;
+        // weights of the first task (and its code range into L2) travel
+        // before the wait on the previous kernel
         if (have) issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, true, false);
     }
     // every layer's x (and y, for write-after-read) belongs to earlier work
     pdl_wait();
-    if (tid == 0 && have) issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, false, true);
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 32 + 30] = gtimer();
+    if (tid == 32) {
+        unsigned long long b;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(b)
+                     : "l"(p.grid_flags + 16 + blockIdx.x)
+                     : "memory");
+        cs.bar_base = b;
+        cs.n_arrive = 0;
+    }
+    int stage = 0;
+    if (tid == 0 && have && p.layer[c.l].stage == 0)
+        issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, false, true);
     if (!(p.flags & kFlagDeterministic)) {
         // zero this CTA's share of every split layer's output, then take the
         // grid ticket (its round trip overlaps the first task)
@@ -922,32 +1039,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (any) {
             __syncthreads();
-            if (tid == 32) {  // arrive (tid 0 is busy issuing the first task's copies)
-                unsigned long long g, old;
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];"
-                             : "=l"(g)
-                             : "l"(p.zero_ticket + 1)
-                             : "memory");
-                cs.zero_gen = g;
-                asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
-                             : "=l"(old)
-                             : "l"(p.zero_ticket)
-                             : "memory");
-                if (old == (unsigned long long)gridDim.x - 1) {
-                    *reinterpret_cast<volatile unsigned long long*>(p.zero_ticket) = 0ull;
-                    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(p.zero_ticket + 1)
-                                 : "memory");
-                }
+            if (tid == 32) {  // arrival 1 (tid 0 is busy issuing the first task's copies)
+                __threadfence();
+                grid_arrive(p, cs);
             }
         }
     }
-    // (all layers of a launch share U: the host splits groups by u)
+    __syncthreads();  // bar_base / n_arrive visible to the CTA
     int buf = 0, task_idx = 0;
     bool first = true;
-    while (have) {
+    while (true) {
+        const int target = have ? p.layer[c.l].stage : p.n_stages - 1;
+        while (stage < target) {  // (CTAs without tasks in a stage still take part)
+            stage_barrier(p, smem_raw, tid);
+            ++stage;
+            if (tid == 0 && have && stage == target)
+                issue_inputs<V, M, U, KB>(p, c, buf, smem_raw, false, true);
+        }
+        if (!have) break;
         TaskCoord nc = c;
         const bool has_next = next_task(p, nc);
-        run_task<V, M, U, KB>(p, c, buf, first, has_next, nc, smem_raw, tid, task_idx++);
+        const bool x_next = has_next && p.layer[nc.l].stage == stage;
+        run_task<V, M, U, KB>(p, c, buf, first, has_next, x_next, nc, smem_raw, tid, task_idx++);
         first = false;
         buf ^= 1;
         c = nc;
@@ -961,26 +1074,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 32 + 31] = gtimer();
 }
 
-// dump the fused kernel's smem Psumbook in _psum_tables layout (m, segs, 2**b, n)
+// dump the fused kernel's smem Psumbook in _psum_tables layout (m, segs, 2**b, n):
+// the same staging and build as the fused kernel, inputs read directly
 template <int V, int M, int U, int KB>
 __global__ void __launch_bounds__(kThreads, 1)
     psumbook_dump_kernel(const DumpParams p, float* __restrict__ out, int64_t segs) {
     using S = FusedShape<V, M, U, KB>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* psum = reinterpret_cast<float*>(smem_raw + p.off_psum);
-    float2* books2 = reinterpret_cast<float2*>(smem_raw + p.off_books);
-    float* x32 = reinterpret_cast<float*>(smem_raw + p.off_x);
+    uint16_t* books16 = reinterpret_cast<uint16_t*>(smem_raw + p.off_books);
+    uint16_t* x16 = reinterpret_cast<uint16_t*>(smem_raw + p.off_x);
     const int tid = threadIdx.x;
     const int64_t slice = blockIdx.x;
     const int col = blockIdx.y;
-    uint16_t breg[S::kBookPerThread];
+    for (int e = tid; e < M * p.kcount * V; e += kThreads) books16[e] = p.books[e];
     uint16_t xreg[S::kXPerThread];
-    load_books<V, M, U, KB>(breg, p.books, p.kcount, tid);
     load_x<V, M, U, KB>(xreg, p.x, slice, p.cols, p.n, col, tid);
-    store_books<V, M, U, KB>(books2, breg, p.kcount, tid);
-    store_x<V, M, U, KB>(x32, xreg, tid);
+    store_x<V, M, U, KB>(x16, xreg, tid);
     __syncthreads();
-    build_psumbook_smem<V, M, U, KB>(psum, books2, x32, p.kcount, tid);
+    build_psumbook_smem<V, M, U, KB>(psum, books16, reinterpret_cast<const uint32_t*>(x16),
+                                     p.kcount, tid);
     __syncthreads();
     const int total = S::kSub * p.kcount * 32;
     for (int i = tid; i < total; i += kThreads) {
@@ -1067,11 +1180,11 @@ cudaError_t launch_group_t(const GroupParams& gp, int grid, int smem, bool pdl, 
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    // owner-mode split-K waits on other CTAs: co-residency guaranteed by a
-    // cooperative launch of a persistent (<= one wave) grid
+    // grid barriers and owner-mode split-K wait on other CTAs: co-residency
+    // guaranteed by a cooperative launch of the persistent (one-wave) grid
     cudaLaunchAttribute attr[2];
     int na = 0;
-    if (!(gp.flags & kFlagLastArriver)) {
+    if (!(gp.flags & kFlagDbgNoCoop)) {
         attr[na].id = cudaLaunchAttributeCooperative;
         attr[na].val.cooperative = 1;
         ++na;
@@ -1110,6 +1223,12 @@ bool visit_vmk(int v, int m, int kb, F&& f) {
     if (m == 3) { CG_KB(V_, 3) }      \
     if (m == 4) { CG_KB(V_, 4) }      \
     return false;
+#ifdef CG_DEV_SUBSET  // fast edit-compile cycles: the two 2-bit headline configs only
+    if (kb != 8) return false;
+    if (v == 4 && m == 1) return f.template run<4, 1, 8>(), true;
+    if (v == 8 && m == 2) return f.template run<8, 2, 8>(), true;
+    return false;
+#else
     switch (v) {
         case 2: { CG_M(2) }
         case 4: { CG_M(4) }
@@ -1117,6 +1236,7 @@ bool visit_vmk(int v, int m, int kb, F&& f) {
         case 16: { CG_M(16) }
         default: return false;
     }
+#endif
 #undef CG_M
 #undef CG_KB
 }
@@ -1149,7 +1269,7 @@ struct SizeQuery {
     template <int V, int M, int U, int KB>
     void run() {
         using S = FusedShape<V, M, U, KB>;
-        z = FusedSizes{S::kPsumBytes, S::kBookBytes, S::kXBytes};
+        z = FusedSizes{S::kPsumBytes, M * S::kCodes * V * 2, S::kXBytes};
     }
 };
 struct GroupLaunch {

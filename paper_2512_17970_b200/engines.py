@@ -253,6 +253,41 @@ def gemm_group(layers, xs, ys=None, stream=None):
     return ys
 
 
+def gemm_stages(layers, xs, ys, stages, stream=None):
+    """One persistent launch running dependent stages of layers (cg_gemm_stages).
+
+    ``stages[i]`` is layer i's stage (0, then non-decreasing by steps of <= 1);
+    layers of one stage are independent, stage s+1 may read what stage s
+    wrote: the kernel orders them with a grid barrier.  ``xs[i]`` is a CUDA
+    (cols_i, n) tensor, float16, or float32 -- typically an earlier stage's y
+    in the same launch -- rounded to binary16 (RNE) as it is read.  ``ys`` are
+    preallocated (rows_i, n) float32 CUDA tensors.  All layers share v, m,
+    code width and tiling u.
+    """
+    import torch
+
+    if not layers or not (len(layers) == len(xs) == len(ys) == len(stages)):
+        raise ShapeError("need one x, y and stage per layer")
+    n = int(xs[0].shape[1])
+    for dl, x, y in zip(layers, xs, ys):
+        if (x.dtype not in (torch.float16, torch.float32) or x.dim() != 2
+                or x.shape[0] != dl.cols or x.shape[1] != n or not x.is_contiguous()):
+            raise ShapeError(f"x for a {dl.rows}x{dl.cols} layer must be contiguous "
+                             f"({dl.cols}, {n}) float16 or float32")
+        if y.dtype != torch.float32 or tuple(y.shape) != (dl.rows, n) or not y.is_contiguous():
+            raise ShapeError(f"y for a {dl.rows}x{dl.cols} layer must be ({dl.rows}, {n}) float32")
+    s = stream if stream is not None else torch.cuda.current_stream(xs[0].device)
+    lib = _lib.load()
+    k = len(layers)
+    hs = (ctypes.c_void_p * k)(*[dl.handle.value for dl in layers])
+    xp = (ctypes.c_void_p * k)(*[x.data_ptr() for x in xs])
+    xd = (ctypes.c_int * k)(*[1 if x.dtype == torch.float32 else 0 for x in xs])
+    yp = (ctypes.c_void_p * k)(*[y.data_ptr() for y in ys])
+    st = (ctypes.c_int * k)(*[int(v) for v in stages])
+    _lib.check(lib.cg_gemm_stages(hs, xp, xd, yp, st, k, n, ctypes.c_void_p(s.cuda_stream)))
+    return ys
+
+
 # one device copy per live layer object (weights are immutable)
 _CACHE: dict = {}
 

@@ -296,3 +296,71 @@ def test_group_launch_default_mode_within_tolerance():
         ys = cg.gemm_group(layers, xs)
         for y, ref in zip(ys, refs):
             assert_within_tolerance(y.cpu().numpy(), ref, "group reduce-add")
+
+
+# ---------------------------------------------------------------- staged launches
+def _chain(shapes, cfg, seed, u, flags=0):
+    layers = [cg.DeviceLayer(cg.random_layer(r, c, cfg, seed=seed + i), u=u, flags=flags)
+              for i, (r, c) in enumerate(shapes)]
+    return layers
+
+
+@pytest.mark.parametrize("det", [True, False])
+def test_staged_chain_matches_separate_launches(det):
+    """x of stage s+1 is y of stage s (float32, rounded to binary16 as read):
+    the in-kernel grid barrier orders it; bit-identical to separate launches
+    on the torch-rounded inputs in deterministic mode, within tolerance in
+    reduce-add mode."""
+    cfg = cg.QuantConfig(v=4, m=1, b=8, g=128)
+    shapes = [(1024, 2048), (4096, 1024), (2048, 4096), (512, 2048)]
+    layers = _chain(shapes, cfg, 300, u=2, flags=DET if det else 0)
+    x0 = cuda_x(orc.bench_input_array(2048, 1, 3))
+    ys = [torch.empty((r, 1), dtype=torch.float32, device="cuda") for r, _ in shapes]
+    xs = [x0] + ys[:-1]
+    for _ in range(3):  # repeated launches: barrier counters carry over
+        for y in ys:
+            y.fill_(float("nan"))
+        cg.gemm_stages(layers, xs, ys, [0, 1, 2, 3])
+        ref_x = x0
+        for dl, y in zip(layers, ys):
+            ref = dl.gemm(ref_x)
+            if det:
+                assert np.array_equal(u32(y.cpu().numpy()), u32(ref.cpu().numpy()))
+            else:
+                assert_within_tolerance(y.cpu().numpy(), ref.cpu().numpy(), "staged chain")
+            ref_x = y.half()  # the next stage's input, as the kernel rounded it
+
+
+def test_staged_block_vs_c_oracle():
+    """Decoder-block chain {q,k,v} -> {o} -> {gate,up} -> {down} in one launch
+    (k/v GQA-shaped), every stage against the C oracle on the fp16-rounded
+    output of the stage before."""
+    cfg = cg.QuantConfig(v=4, m=1, b=8, g=128)
+    H, F, KV = 1024, 3584, 256
+    shapes = [(H, H), (KV, H), (KV, H), (H, H), (F, H), (F, H), (H, F)]
+    stages = [0, 0, 0, 1, 2, 2, 3]
+    qs = [cg.random_layer(r, c, cfg, seed=500 + i) for i, (r, c) in enumerate(shapes)]
+    layers = [cg.DeviceLayer(q, u=2) for q in qs]
+    x0 = orc.bench_input_array(H, 1, 9)
+    ys = [torch.empty((r, 1), dtype=torch.float32, device="cuda") for r, _ in shapes]
+    src = {0: None, 1: None, 2: None, 3: 0, 4: 3, 5: 3, 6: 4}  # x source (layer index)
+    xs = [cuda_x(x0) if src[i] is None else ys[src[i]] for i in range(7)]
+    cg.gemm_stages(layers, xs, ys, stages)
+    got = [y.cpu().numpy() for y in ys]
+    for i, q in enumerate(qs):
+        xin = x0 if src[i] is None else got[src[i]].astype(np.float16)
+        ref = c_oracle.codegemm([p.codes for p in q.planes], [b.entries for b in q.books],
+                                q.scales.scales, xin, 4, 128, threads=8)
+        assert_within_tolerance(got[i], ref, f"block stage layer {i}")
+
+
+def test_staged_launch_rejects_mixed_tiling_and_bad_stages():
+    cfg = cg.QuantConfig(v=4, m=1, b=8, g=128)
+    a = cg.DeviceLayer(cg.random_layer(256, 1024, cfg, seed=1), u=2)
+    b = cg.DeviceLayer(cg.random_layer(256, 1024, cfg, seed=2), u=4)
+    x = cuda_x(orc.bench_input_array(1024, 1, 0))
+    ys = [torch.empty((256, 1), dtype=torch.float32, device="cuda") for _ in range(2)]
+    with pytest.raises(cg.ConfigError):
+        cg.gemm_stages([a, b], [x, x], ys, [0, 1])
+    with pytest.raises(ValueError):
+        cg.gemm_stages([a, a], [x, x], ys, [0, 2])
