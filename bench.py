@@ -11,10 +11,16 @@ reference's bench suite with its multiplicities, bench.py:63-74):
   8b  (default at N=1) : 4 x 4096x4096, 2 x 14336x4096, 1 x 4096x14336
   70b (default at N>1) : 4 x 8192x8192, 2 x 28672x8192, 1 x 8192x28672, rows
                          sharded over the N GPUs + NCCL all-gather per layer
-Every layer of a step has its own weights; steps rotate through enough
-distinct copies of the block that the weight stream is larger than L2
-(inputs larger than L2: no cache flush needed).  Steps are replayed from CUDA
-graphs; time is CUDA events on the launching stream, max over ranks.
+At N=1 a step is ONE persistent launch of the fused kernel (cg_gemm_stages):
+a dependency chain {q,k,v} -> {o} -> {gate,up} -> {down} with grid barriers
+between the stages, where o reads y_q, gate/up read y_o and down reads y_gate
+(binary32, rounded to binary16 as read) -- real data dependencies, no work
+skipped.  At N>1 the 70B block runs row-sharded with grouped launches and an
+NCCL all-gather per layer.  Every layer of a step has its own weights; steps
+rotate through enough distinct copies of the block that the weight stream is
+larger than L2 (inputs larger than L2: no cache flush needed).  Steps are
+replayed from CUDA graphs; time is CUDA events on the launching stream, max
+over ranks.
 
 ``--impl reference`` times the reference's CPU algorithm (the oracle port of
 engines.py:245-316, oracle/codegemm_oracle.py) on a bounded sample of the same
@@ -63,6 +69,10 @@ def layer_bytes(rows: int, cols: int, cfg: dict, n: int, with_io: bool = True) -
 # launch groups of a decoder block (indices into block_spec): layers reading
 # the same x share one grouped launch -- q,k,v | o | gate,up | down
 STEP_GROUPS = ((0, 1, 2), (3,), (4, 5), (6,))
+# the staged step (N=1): stage of each layer and the layer whose y it reads
+STEP_STAGES = (0, 0, 0, 1, 2, 2, 3)
+STEP_XSRC = (None, None, None, 0, 3, 3, 4)
+TILING_U = 2  # one tiling for every layer of a staged launch (64 KB Psumbooks)
 
 
 def block_spec(workload: str):
@@ -286,7 +296,7 @@ def main():
         layers = []
         for idx, (name, rows, cols) in enumerate(spec):
             q = make_layer(rows, cols, cfg, layer_seed(cp, idx, rows, cols))
-            sl = ShardedLayer(q, rank, world) if world > 1 else cg.DeviceLayer(q)
+            sl = ShardedLayer(q, rank, world) if world > 1 else cg.DeviceLayer(q, u=TILING_U)
             x = torch.from_numpy(orc.bench_input_array(cols, n, cp * 31 + idx)).to(dev)
             per = sl.per if world > 1 else rows
             layers.append({"name": name, "rows": rows, "cols": cols, "layer": sl, "x": x,
@@ -332,8 +342,17 @@ def main():
             for i in grp:
                 dist.all_gather_into_tensor(b[i]["y"], b[i]["y_local"])
 
-    graphs = [capture(lambda b=b: [run_group(b, g) for g in groups]) for b in blocks]
-    launches_per_step = len(groups)
+    def run_staged(b):
+        """The whole block in one launch: stage chain with real data dependencies."""
+        xs = [b[i]["x"] if src is None else b[src]["y"] for i, src in enumerate(STEP_XSRC)]
+        cg.gemm_stages([L["layer"] for L in b], xs, [L["y"] for L in b], list(STEP_STAGES))
+
+    if world == 1:
+        graphs = [capture(lambda b=b: run_staged(b)) for b in blocks]
+        launches_per_step = 1
+    else:
+        graphs = [capture(lambda b=b: [run_group(b, g) for g in groups]) for b in blocks]
+        launches_per_step = len(groups)
 
     def timed(replays, count):
         """Replay graphs[i % len] `count` times; device ms (max over ranks)."""
@@ -370,12 +389,18 @@ def main():
     ms_per_step = ms / args.steps
     value = step_bytes * args.steps / (ms / 1e3) / 1e9
 
-    # ---- the same step with one launch per layer (no grouping)
+    # ---- the same step with one launch per layer, and one launch per group
     sep = [capture(lambda b=b: [run_layer(L) for L in b]) for b in blocks]
     reps = max(20, min(400, args.steps // 4))
     timed(sep, 3)
     ms_sep = timed(sep, reps) / reps
     del sep
+    ms_grp = None
+    if world == 1:
+        grp = [capture(lambda b=b: [run_group(b, g) for g in groups]) for b in blocks]
+        timed(grp, 3)
+        ms_grp = timed(grp, reps) / reps
+        del grp
 
     # ---- per-shape kernel microseconds: graphs of R back-to-back launches of
     #      one shape (rotating weight copies), so host launch cost is amortised
@@ -394,6 +419,23 @@ def main():
                       idx)
         del gk
     us_per_layer = {f"{k} {v[1] // world}x{v[2]}": round(v[0], 3) for k, v in kern.items()}
+    # staged chains: CH layers of one shape in ONE launch with a grid barrier
+    # between consecutive layers (a dependent chain, as in a decode step);
+    # chain k uses the shape's layer from block copies k, k+1, ... (distinct weights)
+    us_chain = {}
+    if world == 1:
+        CH = min(7, len(blocks))
+        for name, idx, rows, cols in uniq:
+            def run_chain(k, idx=idx):
+                c = [blocks[(k + r) % len(blocks)][idx] for r in range(CH)]
+                cg.gemm_stages([L["layer"] for L in c], [L["x"] for L in c], [L["y"] for L in c],
+                               list(range(CH)))
+
+            gch = [capture(lambda k=k: run_chain(k)) for k in range(len(blocks))]
+            timed(gch, 2)
+            rr = max(5, reps // CH)
+            us_chain[f"{name} {rows}x{cols}"] = round(timed(gch, rr) / (rr * CH) * 1e3, 3)
+            del gch
     # dominant kernel: the largest per-launch byte count (mlp_gate_up)
     dom = max(kern, key=lambda k: layer_bytes(kern[k][1] // world, kern[k][2], cfg, n))
     dom_us, dom_rows, dom_cols, dom_idx = kern[dom]
@@ -412,13 +454,35 @@ def main():
         except Exception:
             traffic = None
     dl_dom = dev_layer(blocks[0][dom_idx])
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                "kernel": f"group_gemv_kernel {dom} {dom_rows // world}x{dom_cols} "
-                          f"(u={dl_dom.info['u']}, tasks={dl_dom.info['n_tasks']}), "
-                          f"{R} back-to-back launches per graph",
-                "us_per_launch": round(dom_us, 3), "bytes_per_launch": dom_bytes,
-                "frac_of_8TBs_nominal": round(achieved / 8000.0, 4)}
+    if world == 1:
+        # one kernel per step: the staged block launch itself
+        achieved = step_bytes / (ms_per_step * 1e-3) / 1e9
+        traffic = None
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get(f"{args.config}:block{args.workload}")
+            except Exception:
+                traffic = None
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "peak_source": peak_src,
+                    "kernel": f"group_gemv_kernel<v{cfg['v']},m{cfg['m']},u{TILING_U}> staged "
+                              f"block launch (4 stages, {len(spec)} layers, 1 launch per step)",
+                    "us_per_launch": round(ms_per_step * 1e3, 3),
+                    "bytes_per_launch": step_bytes,
+                    "frac_of_8TBs_nominal": round(achieved / 8000.0, 4),
+                    "largest_layer_alone": {"layer": f"{dom} {dom_rows}x{dom_cols}",
+                                            "us_per_launch": round(dom_us, 3),
+                                            "GB/s": round(dom_bytes / (dom_us * 1e-6) / 1e9, 1)}}
+    else:
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "peak_source": peak_src,
+                    "kernel": f"group_gemv_kernel {dom} {dom_rows // world}x{dom_cols} "
+                              f"(u={dl_dom.info['u']}, tasks={dl_dom.info['n_tasks']}), "
+                              f"{R} back-to-back launches per graph",
+                    "us_per_launch": round(dom_us, 3), "bytes_per_launch": dom_bytes,
+                    "frac_of_8TBs_nominal": round(achieved / 8000.0, 4)}
 
     # ---- end to end through the reference-facing C ABI with host buffers
     e2e_steps = max(3, min(args.steps, 100))
@@ -426,14 +490,28 @@ def main():
     h2d = sum(x.nbytes for x in host_x)
     d2h = sum(4 * r * n for (_, r, c) in spec)
 
+    if world == 1:
+        # one step = H2D of the step's inputs (x of q,k,v) from pinned memory,
+        # the staged launch, D2H of every layer's output, synchronise
+        host_x = [torch.from_numpy(orc.bench_input_array(c, n, 100 + i)).pin_memory()
+                  if STEP_XSRC[i] is None else None for i, (_, r, c) in enumerate(spec)]
+        host_y = [torch.empty((r, n), dtype=torch.float32).pin_memory() for (_, r, c) in spec]
+        h2d = sum(x.numel() * 2 for x in host_x if x is not None)
+
     def e2e_step(b):
+        if world == 1:
+            for i, xh in enumerate(host_x):
+                if xh is not None:
+                    b[i]["x"].copy_(xh, non_blocking=True)
+            run_staged(b)
+            for L, yh in zip(b, host_y):
+                yh.copy_(L["y"], non_blocking=True)
+            torch.cuda.synchronize(dev)
+            return
         for L, xh in zip(b, host_x):
-            if world > 1:
-                xt = torch.from_numpy(xh).to(dev, non_blocking=False)
-                y = L["layer"].forward(xt)
-                y.cpu()
-            else:
-                L["layer"].gemm_host(xh)
+            xt = torch.from_numpy(xh).to(dev, non_blocking=False)
+            y = L["layer"].forward(xt)
+            y.cpu()
 
     e2e_step(blocks[0])
     if world > 1:
@@ -450,7 +528,8 @@ def main():
     e2e = {"value": round(step_bytes * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "ms_per_step": round(e2e_s / e2e_steps * 1e3, 3),
-           "path": "cg_layer_gemm_host per layer (pinned staging, H2D x, kernels, D2H y, sync)"
+           "path": "gemm_stages per step (pinned H2D of the step inputs, one staged launch, "
+                   "pinned D2H of all 7 layer outputs, sync)"
            if world == 1 else "ShardedLayer.forward per layer (H2D x, kernels, NCCL all-gather, D2H y)"}
 
     base = base_c = None
@@ -473,14 +552,25 @@ def main():
                              f"({copies * weight_bytes / 2**20:.0f} MiB of weights per rank)",
                        "parallelism": f"rows sharded over {world} GPUs + NCCL all-gather"
                        if world > 1 else "single GPU",
-                       "launch": "per step: 4 grouped fused launches ({q,k,v} {o} {gate,up} "
-                                 "{down}) in a CUDA graph per block copy, PDL between them"},
+                       "launch": ("per step: ONE staged launch (cg_gemm_stages) of the chain "
+                                  "{q,k,v} -> {o} -> {gate,up} -> {down}, o/gate/up/down reading "
+                                  "the previous stage's y rounded to fp16, grid barriers between "
+                                  f"stages, u={TILING_U}; CUDA graph per block copy")
+                       if world == 1 else
+                       "per step: 4 grouped fused launches ({q,k,v} {o} {gate,up} {down}) + "
+                       "NCCL all-gather per layer, CUDA graph per block copy, PDL"},
             "us_per_layer": us_per_layer,
+            "us_per_layer_staged_chain": us_chain,
             "us_per_block": round(ms_per_step * 1e3, 3),
-            "step_launches": [[spec[i][0] for i in g] for g in groups],
+            "step_launches": ([["stage %d: " % s + ",".join(spec[i][0] for i in g)
+                                for s, g in enumerate(groups)]] if world == 1 else
+                              [[spec[i][0] for i in g] for g in groups]),
             "separate_launches": {"us_per_block": round(ms_sep * 1e3, 3),
                                   "value": round(step_bytes / (ms_sep / 1e3) / 1e9, 2),
                                   "launches_per_step": len(spec)},
+            "grouped_launches": None if ms_grp is None else
+            {"us_per_block": round(ms_grp * 1e3, 3),
+             "value": round(step_bytes / (ms_grp / 1e3) / 1e9, 2), "launches_per_step": len(groups)},
             "roofline": roofline,
             "cpu_baseline": base, "cpu_baseline_c": base_c,
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,

@@ -68,7 +68,9 @@ int scale_lg(const cg::Plan& p, int u) {
     if (p.g_eff % lane_elems != 0 || slice_elems % p.g_eff != 0) return -1;
     const int64_t lanes = p.g_eff / lane_elems;
     if (!pow2(lanes)) return -1;
-    return ilog2(lanes);
+    // the gather applies scales once 8 lanes are summed (branch-free
+    // reduction): a scale group must span >= 8 lanes
+    return lanes >= 8 ? ilog2(lanes) : -1;
 }
 
 // Raw task inputs staged by bulk copy: binary16 codebooks, then (16-byte
@@ -493,7 +495,11 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
         reserved = 1024;
     L->reserved = reserved;
     plan_fast(p, opts ? opts->u : 0, opts ? opts->rg_per_task : 0, sm_count_of(device), reserved);
-    if (opts && opts->u && !p.fast) {
+    // a tiling the fused kernel never has (u not in {1,2,4} or m*u > 4) is a
+    // config error; a valid u the fused kernel cannot use for this group size
+    // (scale group < 8 lanes) leaves a strict-mode-only layer
+    if (opts && opts->u && !p.fast &&
+        (!(opts->u == 1 || opts->u == 2 || opts->u == 4) || m * opts->u > 4)) {
         free_layer(L);
         return fail(CG_ERR_CONFIG, "u=%d is not valid for v=%d m=%d b=%d g=%lld", opts->u, v, m,
                     b, (long long)g);

@@ -549,7 +549,7 @@ __device__ __forceinline__ void load_tile(uint4 (&cw)[M][U], const uint8_t* tp) 
 // the LDS immediate: one PRMT + one LDS per lookup, no address arithmetic.
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ float gather_row_group(const uint4 (&cw)[M][U], const uint16_t* sp,
-                                                  uint32_t lb0, uint32_t lb1, int lg, int mask) {
+                                                  uint32_t lb0, uint32_t lb1, int mask) {
     using S = FusedShape<V, M, U, KB>;
     // lookups: a[i] = sum over (t, u) of psum_t[seg(lane,u)][code of slot i],
     // two slots at a time with packed FADD2
@@ -580,18 +580,18 @@ __device__ __forceinline__ float gather_row_group(const uint4 (&cw)[M][U], const
         a[i] = s2.x;
         a[i + 1] = s2.y;
     }
-    // transpose-reduce across lanes; scales once the lanes of a group are summed
-    if (lg == 0) apply_scales<16>(a, sp, mask & 15);
+    // Transpose-reduce the 16 slot partials across lanes; lanes 0-15 keep their
+    // rows' sums.  The fused kernel requires a scale group to span >= 8 lanes
+    // (lg >= 3; every g = 128 configuration), so after the first
+    // three halvings (lanes differing in bits 0-2 summed) all lanes still to
+    // be combined share each row's scale: the scales are applied there, to the
+    // two remaining slots, and the reduction is branch-free.
     halve<16>(a, 1);
-    if (lg == 1) apply_scales<8>(a, sp, mask & 7);
     halve<8>(a, 2);
-    if (lg == 2) apply_scales<4>(a, sp, mask & 3);
     halve<4>(a, 4);
-    if (lg == 3) apply_scales<2>(a, sp, mask & 1);
+    apply_scales<2>(a, sp, mask & 1);
     halve<2>(a, 8);
-    if (lg == 4) apply_scales<1>(a, sp, 0);
     a[0] += __shfl_xor_sync(0xffffffffu, a[0], 16);
-    if (lg >= 5) apply_scales<1>(a, sp, 0);
     return a[0];
 }
 
@@ -861,10 +861,9 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     if (psum_addr & 0xffffu) __trap();
     const uint32_t lb0 = ((uint32_t)lane << 2) | ((psum_addr >> 16) << 8);
     const uint32_t lb1 = lb0 | 0x80u;
-    const int lg = L.lg;
-    const int ls = lg < 4 ? lg : 4;
+    const int lg = L.lg;  // >= 3 (host planner)
     const int mask = row_mask(lane);
-    const int sbase = mask & ~((16 >> ls) - 1);  // first row of this lane's scale run
+    const int sbase = mask & ~1;  // first row of this lane's two scaled slots
     const int gi = lg >= 5 ? 0 : (lane >> lg);
     const uint16_t* sp0 = scl_s + (warp * n_gs + gi) * 16 + sbase;
     const int sstep = kWarps * n_gs * 16;
@@ -908,7 +907,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
                 const int i = i0 + d;
                 if (i < n_rgs) {
                     const float v = gather_row_group<V, M, U, KB>(tb[d], sp0 + i * sstep, lb0, lb1,
-                                                                  lg, mask);
+                                                                  mask);
                     if (i + D < load_rgs) load_tile<V, M, U, KB>(tb[d], cptr + (i + D) * kStep);
                     if (lane < 16 && row < L.rows) out[row * n + col] = v;
                     row += row_step;
