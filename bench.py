@@ -347,23 +347,52 @@ def main():
         xs = [b[i]["x"] if src is None else b[src]["y"] for i, src in enumerate(STEP_XSRC)]
         cg.gemm_stages([L["layer"] for L in b], xs, [L["y"] for L in b], list(STEP_STAGES))
 
+    CHAIN = int(os.environ.get("CG_BENCH_CHAIN", "2"))  # blocks per launch (<= 16 layers)
+
+    def run_staged_chain(j0):
+        """CHAIN block copies, chained, in ONE persistent launch: block j's q,k,v read
+        block j-1's y_down (a model's layer stack), stages 4j .. 4j+3."""
+        lay, xs, ys, st = [], [], [], []
+        for jj in range(CHAIN):
+            j = (j0 + jj) % len(blocks)
+            b = blocks[j]
+            for i, src in enumerate(STEP_XSRC):
+                lay.append(b[i]["layer"])
+                if src is not None:
+                    xs.append(b[src]["y"])
+                else:
+                    xs.append(b[i]["x"] if jj == 0 else blocks[(j - 1) % len(blocks)][len(spec) - 1]["y"])
+                ys.append(b[i]["y"])
+                st.append(len(groups) * jj + STEP_STAGES[i])
+        cg.gemm_stages(lay, xs, ys, st)
+
     if world == 1:
-        graphs = [capture(lambda b=b: run_staged(b)) for b in blocks]
-        launches_per_step = 1
+        # one launch runs a step for every block copy (len(blocks) decoder
+        # blocks chained: launch and grid-completion latency are paid once per
+        # copy cycle); single-step launches make up a step count that is not
+        # a multiple of the copy count
+        nlaunch = len(blocks) // CHAIN
+        graphs = [capture(lambda: [run_staged_chain(CHAIN * k) for k in range(nlaunch)])]
+        singles = [capture(lambda b=b: run_staged(b)) for b in blocks]
+        launches_per_step = 1.0 / CHAIN
     else:
         graphs = [capture(lambda b=b: [run_group(b, g) for g in groups]) for b in blocks]
+        singles = None
         launches_per_step = len(groups)
 
-    def timed(replays, count):
-        """Replay graphs[i % len] `count` times; device ms (max over ranks)."""
+    def timed(replays, count, per_graph=1):
+        """Replay graphs[i % len] until `count` steps (per_graph steps per replay) ran;
+        device ms (max over ranks)."""
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             ev0.record(stream)
-            for i in range(count):
+            for i in range(count // per_graph):
                 replays[i % len(replays)].replay()
+            for i in range(count % per_graph):  # exactly `count` steps
+                singles[i].replay()
             ev1.record(stream)
         torch.cuda.synchronize(dev)
         ms = ev0.elapsed_time(ev1)
@@ -375,13 +404,14 @@ def main():
         return ms
 
     # ---- warmup + timed region (clocks sampled during it)
-    timed(graphs, args.warmup)
+    spg = (len(blocks) // CHAIN) * CHAIN if world == 1 else 1  # steps per graph replay
+    timed(graphs, args.warmup, spg)
     soak = 0
     with ClockSampler(local_rank) as clk:
-        ms = timed(graphs, args.steps)
+        ms = timed(graphs, args.steps, spg)
         if ms < 1000.0:  # too short for 50 ms sampling: keep the same load running ~1 s
             soak = int(args.steps * (1000.0 - ms) / max(ms, 1e-3)) + 1
-            timed(graphs, soak)
+            timed(graphs, soak, spg)
     clocks = clk.summary()
     if clocks is not None and soak:
         clocks["note"] = (f"timed region {ms:.1f} ms; sampling continued over {soak} more "
@@ -390,16 +420,18 @@ def main():
     value = step_bytes * args.steps / (ms / 1e3) / 1e9
 
     # ---- the same step with one launch per layer, and one launch per group
-    sep = [capture(lambda b=b: [run_layer(L) for L in b]) for b in blocks]
     reps = max(20, min(400, args.steps // 4))
-    timed(sep, 3)
-    ms_sep = timed(sep, reps) / reps
+    reps = -(-reps // spg) * spg
+    sep = [capture(lambda: [run_layer(L) for b in blocks for L in b])] if world == 1 else \
+        [capture(lambda b=b: [run_layer(L) for L in b]) for b in blocks]
+    timed(sep, 3 * spg, spg)
+    ms_sep = timed(sep, reps, spg) / reps
     del sep
     ms_grp = None
     if world == 1:
-        grp = [capture(lambda b=b: [run_group(b, g) for g in groups]) for b in blocks]
-        timed(grp, 3)
-        ms_grp = timed(grp, reps) / reps
+        grp = [capture(lambda: [run_group(b, g) for b in blocks for g in groups])]
+        timed(grp, 3 * spg, spg)
+        ms_grp = timed(grp, reps, spg) / reps
         del grp
 
     # ---- per-shape kernel microseconds: graphs of R back-to-back launches of
@@ -431,10 +463,11 @@ def main():
                 cg.gemm_stages([L["layer"] for L in c], [L["x"] for L in c], [L["y"] for L in c],
                                list(range(CH)))
 
-            gch = [capture(lambda k=k: run_chain(k)) for k in range(len(blocks))]
-            timed(gch, 2)
-            rr = max(5, reps // CH)
-            us_chain[f"{name} {rows}x{cols}"] = round(timed(gch, rr) / (rr * CH) * 1e3, 3)
+            gch = [capture(lambda: [run_chain(k) for k in range(len(blocks))])]
+            nb = len(blocks)
+            timed(gch, 2 * nb, nb)
+            rr = max(2, reps // (CH * nb)) * nb
+            us_chain[f"{name} {rows}x{cols}"] = round(timed(gch, rr, nb) / (rr * CH) * 1e3, 3)
             del gch
     # dominant kernel: the largest per-launch byte count (mlp_gate_up)
     dom = max(kern, key=lambda k: layer_bytes(kern[k][1] // world, kern[k][2], cfg, n))
@@ -467,7 +500,8 @@ def main():
                     "frac": round(achieved / peak, 4), "traffic": traffic,
                     "peak_source": peak_src,
                     "kernel": f"group_gemv_kernel<v{cfg['v']},m{cfg['m']},u{TILING_U}> staged "
-                              f"block launch (4 stages, {len(spec)} layers, 1 launch per step)",
+                              f"launch, {CHAIN} chained blocks ({CHAIN * len(spec)} "
+                              f"layers, {CHAIN * len(groups)} stages); per-step share",
                     "us_per_launch": round(ms_per_step * 1e3, 3),
                     "bytes_per_launch": step_bytes,
                     "frac_of_8TBs_nominal": round(achieved / 8000.0, 4),
@@ -552,10 +586,12 @@ def main():
                              f"({copies * weight_bytes / 2**20:.0f} MiB of weights per rank)",
                        "parallelism": f"rows sharded over {world} GPUs + NCCL all-gather"
                        if world > 1 else "single GPU",
-                       "launch": ("per step: ONE staged launch (cg_gemm_stages) of the chain "
-                                  "{q,k,v} -> {o} -> {gate,up} -> {down}, o/gate/up/down reading "
-                                  "the previous stage's y rounded to fp16, grid barriers between "
-                                  f"stages, u={TILING_U}; CUDA graph per block copy")
+                       "launch": ("one persistent staged launch (cg_gemm_stages) per "
+                                  f"{CHAIN} steps: {CHAIN} block copies chained "
+                                  "as a layer stack, each block the stages {q,k,v} -> {o} -> "
+                                  "{gate,up} -> {down}; o/gate/up/down read the previous stage's "
+                                  "y and the next block's q,k,v read y_down, rounded to fp16; "
+                                  f"grid barriers between stages, u={TILING_U}; CUDA graph")
                        if world == 1 else
                        "per step: 4 grouped fused launches ({q,k,v} {o} {gate,up} {down}) + "
                        "NCCL all-gather per layer, CUDA graph per block copy, PDL"},
@@ -573,7 +609,9 @@ def main():
              "value": round(step_bytes / (ms_grp / 1e3) / 1e9, 2), "launches_per_step": len(groups)},
             "roofline": roofline,
             "cpu_baseline": base, "cpu_baseline_c": base_c,
-            "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "e2e": e2e,
+            "gpu_launches": (args.steps // spg * (spg // CHAIN) + args.steps % spg) if world == 1
+            else launches_per_step * args.steps,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

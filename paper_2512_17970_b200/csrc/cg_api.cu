@@ -147,6 +147,7 @@ void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms, int reserved) {
         if (cost < best) {
             best = cost;
             p.fast = true;
+            p.rg_cap = (int)rg_cap;
             p.u = u;
             p.lg = lg;
             p.n_gs = 32 >> lg;
@@ -189,6 +190,8 @@ struct cg_layer {
     int flags = 0;
     int pf_dist = 0;
     int sms = 148;
+    bool rg_forced = false;  // rg_per_task given at creation: launches keep the task split
+    int rg_cap = 0;          // largest rows-per-task whose task buffers fit shared memory (n=1)
     unsigned long long* stamps = nullptr;  // diagnostics (CG_STAMPS=1)
     int64_t device_bytes = 0;
 };
@@ -329,15 +332,66 @@ int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* con
         zmax.psum = std::max(zmax.psum, z.psum);
         zmax.books = std::max(zmax.books, z.books);
         zmax.x = std::max(zmax.x, z.x);
-        scl_max = std::max(scl_max, p.rg_per_task * p.n_gs * 32);
-        rg_max = std::max(rg_max, p.rg_per_task);
-        grid = std::max(grid, gp.layer[i].n_tasks);
         raw_bytes = std::max(raw_bytes, raw_input_bytes(p, p.u));
         books_raw = std::max(books_raw, raw_books_bytes(p));
         // x travels by bulk copy only if every slice of it is a 16-byte multiple
         if ((reinterpret_cast<uintptr_t>(xs[i]) & 15) || (p.cols % 8)) x_copy = false;
     }
     gp.n_stages = prev_stage + 1;
+    // ---- per-stage task split.  A layer's plan fills the GPU on its own
+    //      (~1 task per SM); a stage of several layers would then run several
+    //      tasks -- several Psumbook builds -- per CTA.  Re-split the rows of
+    //      the stage's layers jointly (the prepacked layout does not depend on
+    //      it): minimise waves x (per-task cost + rows per task), the per-task
+    //      cost (table build, input round trip, flush) expressed in row groups
+    //      of gather work.  Layers created with an explicit rg_per_task keep it.
+    {
+        const int sms = layers[0]->sms;
+        bool forced = false;
+        int64_t cap = 1 << 30;
+        for (int i = 0; i < count; ++i) {
+            forced |= layers[i]->rg_forced;
+            cap = std::min<int64_t>(cap, layers[i]->rg_cap / n);
+        }
+        if (!forced) {
+            for (int st = 0; st < gp.n_stages; ++st) {
+                int64_t max_rg = 1;
+                for (int i = 0; i < count; ++i)
+                    if (gp.layer[i].stage == st) max_rg = std::max(max_rg, gp.layer[i].n_rg);
+                const double f_rg = 2.0 / (0.019 * p0.u * p0.m);  // ~2 us of fixed cost per task
+                double best = 1e300;
+                int64_t best_rg = 0;
+                for (int64_t rg = 1; rg <= max_rg; ++rg) {
+                    if (rg > cap) break;
+                    int64_t tasks = 0;
+                    for (int i = 0; i < count; ++i)
+                        if (gp.layer[i].stage == st)
+                            tasks += gp.layer[i].n_slices * ((gp.layer[i].n_rg + rg - 1) / rg);
+                    const double waves = (double)((tasks + sms - 1) / sms);
+                    const double cost = waves * (f_rg + (double)rg) + 1e-6 * (double)rg;
+                    if (cost < best) {
+                        best = cost;
+                        best_rg = rg;
+                    }
+                }
+                if (best_rg < 1) continue;
+                for (int i = 0; i < count; ++i) {
+                    cg::LayerTask& t = gp.layer[i];
+                    if (t.stage != st) continue;
+                    const int64_t rg = std::min<int64_t>(best_rg, t.n_rg);
+                    t.rg_per_task = (int)rg;
+                    t.n_rb = (t.n_rg + rg - 1) / rg;
+                    t.n_tasks = (int)(t.n_slices * t.n_rb);
+                }
+            }
+        }
+        for (int i = 0; i < count; ++i) {
+            const cg::Plan& p = layers[i]->plan;
+            scl_max = std::max(scl_max, gp.layer[i].rg_per_task * p.n_gs * 32);
+            rg_max = std::max(rg_max, gp.layer[i].rg_per_task);
+            grid = std::max(grid, gp.layer[i].n_tasks);
+        }
+    }
     // persistent grid: one CTA per SM, always the full grid (the per-CTA grid
     // barrier flags rely on every launch making the same arrivals on every
     // CTA); if a layer has more tasks than CTAs, a CTA runs several tasks of it
@@ -495,6 +549,8 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
         reserved = 1024;
     L->reserved = reserved;
     plan_fast(p, opts ? opts->u : 0, opts ? opts->rg_per_task : 0, sm_count_of(device), reserved);
+    L->rg_forced = opts && opts->rg_per_task > 0;
+    L->rg_cap = p.fast ? p.rg_cap : 0;
     // a tiling the fused kernel never has (u not in {1,2,4} or m*u > 4) is a
     // config error; a valid u the fused kernel cannot use for this group size
     // (scale group < 8 lanes) leaves a strict-mode-only layer
@@ -571,8 +627,8 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
         cudaMemset(L->grid_flags, 0, fb);
     }
     if (p.fast && std::getenv("CG_STAMPS")) {
-        if ((rc = dev_alloc(L, &L->stamps, (size_t)L->sms * 256, "stamps"))) return bail(rc);
-        cudaMemset(L->stamps, 0, (size_t)L->sms * 256);
+        if ((rc = dev_alloc(L, &L->stamps, (size_t)L->sms * 512, "stamps"))) return bail(rc);
+        cudaMemset(L->stamps, 0, (size_t)L->sms * 512);
     }
     *out = L;
     return CG_OK;
@@ -726,7 +782,7 @@ int cg_psumbook_build(const void* books, const void* x, int m, int b, int v, int
 extern "C" int cg_debug_stamps(cg_layer* L, unsigned long long* host, int64_t count) {
     if (!L || !L->stamps) return fail(CG_ERR_ARG, "no stamps (set CG_STAMPS=1)");
     DeviceGuard guard(L->device);
-    const int64_t n = std::min<int64_t>(count, (int64_t)L->sms * 32);
+    const int64_t n = std::min<int64_t>(count, (int64_t)L->sms * 64);
     CG_CUDA(cudaMemcpy(host, L->stamps, n * 8, cudaMemcpyDeviceToHost), "stamps D2H");
     return CG_OK;
 }

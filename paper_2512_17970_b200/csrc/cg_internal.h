@@ -108,7 +108,7 @@ inline bool smem_layout(const FusedSizes& z, int scl_bytes, int raw_bytes, int l
                         int reserved, SmemLayout* L, int stage_bytes = 0) {
     auto up = [](int v, int a) { return (v + a - 1) / a * a; };
     const int kMax = 227 * 1024;
-    const int kState = 128;  // CtaState
+    const int kState = 1024;  // CtaState (incl. the CTA's task list)
     struct Piece {
         int* off;
         int size;
@@ -163,6 +163,7 @@ struct Plan {
     int lg = 0;               // log2(lanes per scale group), 0..5
     int n_gs = 0;             // scale groups per slice tile = 32 >> lg
     int rg_per_task = 0;
+    int rg_cap = 0;           // largest rg_per_task whose task buffers fit shared memory
     int64_t n_rb = 0;         // row blocks (tasks per slice)
     int64_t code_bytes = 0;   // prepacked code stream
     int64_t scale_bytes = 0;  // prepacked scale tiles

@@ -222,7 +222,7 @@ struct FusedShape {
     #ifdef CG_NOHOIST
     static constexpr bool kHoist = false;
 #else
-    static constexpr bool kHoist = kCPT * V <= 32;
+    static constexpr bool kHoist = kCPT * V <= 16;
 #endif
     // register pipeline depth of the code-tile stream (tiles of 16*M*U bytes per lane)
     #ifdef CG_DEPTH
@@ -623,6 +623,7 @@ struct FixupEntry {
 // mbarrier, the fix-up count, the previous task (closed at the start of the
 // next task, after that task's input loads are in flight, or at kernel end)
 // and the zero-barrier generation.
+constexpr int kTaskList = 48;
 struct CtaState {
     uint64_t in_bar[2];           // mbarriers of the two task-input buffers
     int list_count;
@@ -633,6 +634,11 @@ struct CtaState {
     int prev_layer;
     long long prev_slice, prev_rg0, prev_rg1;
     int n_bar;                    // stage barriers passed (diagnostics)
+    // this CTA's task list, enumerated once at kernel start (task switches
+    // must not walk the layer table: indexed parameter loads are slow)
+    int n_tl;                     // entries (kTaskList = more tasks follow)
+    int tl_l[kTaskList], tl_g[kTaskList];
+    long long tl_t[kTaskList];
 };
 struct PrevTask {
     int layer;
@@ -640,22 +646,23 @@ struct PrevTask {
 };
 
 // ---- grid barriers: one monotonic arrival counter ----
-// grid_flags[0] counts barrier arrivals of all CTAs over all launches that used
-// this array; grid_flags[16 + c] (another cache line) is CTA c's own arrival
-// count, read at launch start.  Every such launch runs the full grid and every
-// CTA makes the same arrivals, so at launch start counter = grid * own.
-// Arrival k is a release reduction (fire-and-forget, no contended round trip);
-// waiting for arrival k polls the counter until it reaches grid * (own + k).
-__device__ __forceinline__ void grid_arrive(const GroupParams& p, CtaState& cs) {
-    ++cs.n_arrive;
-    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(p.grid_flags) : "memory");
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.grid_flags + 16 + blockIdx.x),
-                 "l"(cs.bar_base + (unsigned long long)cs.n_arrive)
+// grid_flags[0] counts arrival units of all CTAs over all launches that used
+// this array; grid_flags[16 + c] (another cache line) is CTA c's own count,
+// written at kernel end and read at the next launch's start.  Every such
+// launch runs the full grid and every CTA arrives kBarUnits units per barrier,
+// so at launch start counter = grid * own.  An arrival is a release reduction
+// (fire-and-forget: no contended round trip); barrier k is passed once the
+// counter reaches grid * (own + kBarUnits * k).
+constexpr int kBarUnits = kWarps;  // the zero barrier: one unit per warp
+__device__ __forceinline__ void grid_red(const GroupParams& p, unsigned units) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p.grid_flags),
+                 "l"((unsigned long long)units)
                  : "memory");
 }
 // one thread; returns once every CTA made arrival k
 __device__ __forceinline__ void grid_wait(const GroupParams& p, const CtaState& cs, int k) {
-    const unsigned long long want = (cs.bar_base + (unsigned long long)k) * gridDim.x;
+    const unsigned long long want =
+        (cs.bar_base + (unsigned long long)kBarUnits * (unsigned long long)k) * gridDim.x;
     unsigned long long f;
     while (true) {
         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(p.grid_flags) : "memory");
@@ -737,18 +744,48 @@ __device__ void close_task(const GroupParams& p, unsigned char* smem_raw, int ti
 // ---- task inputs: raw codebooks + x slice + scale tiles by TMA bulk copies
 // into one of two smem buffers (double-buffered across tasks), so the next
 // task's inputs travel while the current task gathers.
+// A task is (layer l, task t of that layer).  Within a stage the tasks of
+// all its layers are numbered consecutively (layer order) and CTA c runs
+// numbers c, c + grid, ...; g is that stage-wide number.
 struct TaskCoord {
     int l;
     int64_t t;
+    int64_t g;
 };
 
-__device__ __forceinline__ bool next_task(const GroupParams& p, TaskCoord& c) {
-    c.t += gridDim.x;
-    while (c.l < p.n_layers && c.t >= p.layer[c.l].n_tasks) {
-        ++c.l;
-        c.t = blockIdx.x;
+// first layer index of stage s (layers are sorted by stage), n_layers if none
+__device__ __forceinline__ int stage_first(const GroupParams& p, int s) {
+    int l = 0;
+    while (l < p.n_layers && p.layer[l].stage < s) ++l;
+    return l;
+}
+
+// stage-wide task number g of stage s -> (l, t); false if g is past the stage
+__device__ __forceinline__ bool locate(const GroupParams& p, int s, int64_t g, TaskCoord& c) {
+    int l = stage_first(p, s);
+    int64_t r = g;
+    while (l < p.n_layers && p.layer[l].stage == s && r >= p.layer[l].n_tasks) {
+        r -= p.layer[l].n_tasks;
+        ++l;
     }
-    return c.l < p.n_layers;
+    if (l >= p.n_layers || p.layer[l].stage != s) return false;
+    c.l = l;
+    c.t = r;
+    c.g = g;
+    return true;
+}
+
+// this CTA's first task in stage s or later
+__device__ __forceinline__ bool first_task_from(const GroupParams& p, int s, TaskCoord& c) {
+    for (; s < p.n_stages; ++s)
+        if (locate(p, s, (int64_t)blockIdx.x, c)) return true;
+    return false;
+}
+
+__device__ __forceinline__ bool next_task(const GroupParams& p, TaskCoord& c) {
+    const int s = p.layer[c.l].stage;
+    if (locate(p, s, c.g + gridDim.x, c)) return true;
+    return first_task_from(p, s + 1, c);
 }
 
 __device__ __forceinline__ bool x_by_copy(const GroupParams& p, const LayerTask& L) {
@@ -818,7 +855,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem_raw + p.off_raw[buf]);
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
     unsigned long long* stamps =
-        (p.stamps && task_idx < 3) ? p.stamps + blockIdx.x * 32 + task_idx * 8 : nullptr;
+        (p.stamps && task_idx < 6) ? p.stamps + blockIdx.x * 64 + task_idx * 8 : nullptr;
 #define CG_STAMP(k) \
     if (stamps && tid == 0) stamps[k] = gtimer();
 
@@ -958,15 +995,17 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
     __syncthreads();
     close_task(p, smem_raw, tid);  // deterministic split-K: pending ordered sums
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
-    unsigned long long* st = p.stamps ? p.stamps + blockIdx.x * 32 + 24 : nullptr;
-    const bool first_bar = cs.n_bar == 0;  // stamps of the first barrier only
+    unsigned long long* st =
+        (p.stamps && cs.n_bar < 3) ? p.stamps + blockIdx.x * 64 + 48 + 4 * cs.n_bar : nullptr;
+    const bool first_bar = true;  // (stamps of the first three barriers)
     if (tid == 0) {
         if (st && first_bar) st[0] = gtimer();
         cs.prev_layer = -1;
         bulk_wait_all();
         asm volatile("fence.proxy.async.global;" ::: "memory");
         if (st && first_bar) st[1] = gtimer();
-        grid_arrive(p, cs);
+        ++cs.n_arrive;
+        grid_red(p, kBarUnits);
         if (st && first_bar) st[2] = gtimer();
         grid_wait(p, cs, cs.n_arrive);
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -990,13 +1029,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (p.flags & kFlagDbgEmpty) return;
     const int tid = threadIdx.x;
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 64 + 60] = gtimer();
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
-    TaskCoord c{0, (int64_t)blockIdx.x};
-    while (c.l < p.n_layers && c.t >= p.layer[c.l].n_tasks) {
-        ++c.l;
-        c.t = blockIdx.x;
-    }
-    bool have = c.l < p.n_layers;
+    TaskCoord c{0, 0, 0};
+    bool have = first_task_from(p, 0, c);
     if (tid == 0) {
         mbar_init(&cs.in_bar[0], 1);
         mbar_init(&cs.in_bar[1], 1);
@@ -1008,11 +1044,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         // weights of the first task (and its code range into L2) travel
         // before the wait on the previous kernel
         if (have) issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, true, false);
+        int cnt = 0;
+        if (have) {
+            TaskCoord e = c;
+            bool more = true;
+            while (more && cnt < kTaskList) {
+                cs.tl_l[cnt] = e.l;
+                cs.tl_t[cnt] = e.t;
+                cs.tl_g[cnt] = (int)e.g;
+                ++cnt;
+                more = next_task(p, e);
+            }
+            cs.n_tl = more ? kTaskList + 1 : cnt;  // kTaskList + 1: list full, more follow
+        } else {
+            cs.n_tl = 0;
+        }
     }
     // every layer's x (and y, for write-after-read) belongs to earlier work
     pdl_wait();
-    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 32 + 30] = gtimer();
-    if (tid == 32) {
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 64 + 62] = gtimer();
+    if (tid == 0) {  // (barrier state is used by thread 0 only)
         unsigned long long b;
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(b)
                      : "l"(p.grid_flags + 16 + blockIdx.x)
@@ -1024,9 +1075,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0 && have && p.layer[c.l].stage == 0)
         issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, false, true);
     if (!(p.flags & kFlagDeterministic)) {
-        // zero this CTA's share of every split layer's output, then take the
-        // grid ticket (its round trip overlaps the first task)
+        // zero this CTA's share of every split layer's output; each warp
+        // releases its own stores (arrival 1: one unit per warp), so no CTA
+        // barrier sits on this path -- the first flush waits for the grid
         bool any = false;
+        const int warp = tid >> 5, lane = tid & 31;
         for (int l = 0; l < p.n_layers; ++l) {
             const LayerTask& L = p.layer[l];
             if (L.n_slices <= 1) continue;
@@ -1037,14 +1090,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int64_t e = e0 + tid; e < e1; e += kThreads) L.y[e] = 0.0f;
         }
         if (any) {
-            __syncthreads();
-            if (tid == 32) {  // arrival 1 (tid 0 is busy issuing the first task's copies)
-                __threadfence();
-                grid_arrive(p, cs);
-            }
+            __syncwarp();
+            if (lane == 0) grid_red(p, 1);  // release: orders the warp's zero stores
+            if (tid == 0) cs.n_arrive = 1;
+            (void)warp;
         }
     }
-    __syncthreads();  // bar_base / n_arrive visible to the CTA
+    __syncthreads();  // CTA state (task list, mbarriers) visible to every thread
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 64 + 61] = gtimer();
     int buf = 0, task_idx = 0;
     bool first = true;
     while (true) {
@@ -1057,7 +1110,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!have) break;
         TaskCoord nc = c;
-        const bool has_next = next_task(p, nc);
+        bool has_next;
+        if (task_idx + 1 < min(cs.n_tl, kTaskList)) {
+            nc.l = cs.tl_l[task_idx + 1];
+            nc.t = cs.tl_t[task_idx + 1];
+            nc.g = cs.tl_g[task_idx + 1];
+            has_next = true;
+        } else if (cs.n_tl <= kTaskList && task_idx + 1 >= cs.n_tl) {
+            has_next = false;
+        } else {
+            has_next = next_task(p, nc);  // beyond the enumerated list (rare)
+        }
         const bool x_next = has_next && p.layer[nc.l].stage == stage;
         run_task<V, M, U, KB>(p, c, buf, first, has_next, x_next, nc, smem_raw, tid, task_idx++);
         first = false;
@@ -1068,9 +1131,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // close the last task's row groups; drain the bulk reduce-adds
     __syncthreads();
     close_task(p, smem_raw, tid);
-    if (tid == 0) bulk_wait_all();
+    if (tid == 0) {
+        bulk_wait_all();
+        // this CTA's arrival count for the next launch on these flags
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.grid_flags + 16 + blockIdx.x),
+                     "l"(cs.bar_base + (unsigned long long)kBarUnits * cs.n_arrive)
+                     : "memory");
+    }
     __syncthreads();
-    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 32 + 31] = gtimer();
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 64 + 63] = gtimer();
 }
 
 // dump the fused kernel's smem Psumbook in _psum_tables layout (m, segs, 2**b, n):

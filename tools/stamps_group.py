@@ -41,14 +41,14 @@ lib = _lib.load()
 lib.cg_debug_stamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
 bufs = []
 for k in range(2):
-    buf = np.zeros(sms * 32, dtype=np.uint64)
-    _lib.check(lib.cg_debug_stamps(sets[k][0].handle, buf.ctypes.data, sms * 32))
-    bufs.append(buf.reshape(sms, 32).astype(np.int64))
+    buf = np.zeros(sms * 64, dtype=np.uint64)
+    _lib.check(lib.cg_debug_stamps(sets[k][0].handle, buf.ctypes.data, sms * 64))
+    bufs.append(buf.reshape(sms, 64).astype(np.int64))
 prev, st = bufs[0], bufs[1]  # launch 4 (set 0) then launch 5 (set 1)
 valid = st[:, 0] > 0
 t0 = st[valid, 0].min()
 print(sets[0][0].info)
-pend = prev[prev[:, 31] > 0, 31]
+pend = prev[prev[:, 63] > 0, 63]
 print(f"previous launch: last CTA end {(pend.max() - t0) / 1e3:7.2f} us (rel. to this launch's first start)")
 
 
@@ -59,12 +59,12 @@ def show(name, col):
         print(f"{name:18s} min {r.min():7.2f} med {np.median(r):7.2f} max {r.max():7.2f}")
 
 
-show("pdl_wait passed", st[valid, 30])
+show("pdl_wait passed", st[valid, 62])
 names = [(0, "start"), (7, "synced"), (4, "inputs ok"), (5, "x staged"), (6, "built"),
          (1, "gathered"), (2, "zero barrier ok"), (3, "task end")]
 for k in range(min(count, 3)):
     for slot, nm in names:
         show(f"task{k} {nm}", st[valid, k * 8 + slot])
-for slot, nm in ((24, "barrier entered"), (25, "bulk drained"), (26, "arrived"), (27, "released")):
+for slot, nm in ((48, "barrier entered"), (49, "bulk drained"), (50, "arrived"), (51, "released")):
     show(nm, st[valid, slot])
-show("kernel end", st[valid, 31])
+show("kernel end", st[valid, 63])
