@@ -347,7 +347,7 @@ def main():
         xs = [b[i]["x"] if src is None else b[src]["y"] for i, src in enumerate(STEP_XSRC)]
         cg.gemm_stages([L["layer"] for L in b], xs, [L["y"] for L in b], list(STEP_STAGES))
 
-    CHAIN = int(os.environ.get("CG_BENCH_CHAIN", "2"))  # blocks per launch (<= 16 layers)
+    CHAIN = int(os.environ.get("CG_BENCH_CHAIN", "1"))  # blocks per launch (<= 16 layers)
 
     def run_staged_chain(j0):
         """CHAIN block copies, chained, in ONE persistent launch: block j's q,k,v read

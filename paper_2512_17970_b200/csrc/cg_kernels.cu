@@ -196,8 +196,8 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed,
 //
 // The centroids of a thread's codes are read once per codebook straight from
 // the raw binary16 codebook buffer (TMA-staged) and kept in registers across
-// the U sub-tables; x is staged once per task as binary16 pairs in the layout
-// the FFMA2 operands want (x16_word), 16-byte skewed per lane quad so the 8
+// the U sub-tables; x is staged once per task as binary32 pairs in the layout
+// the FFMA2 operands want (x_index), 16-byte skewed per lane quad so the 8
 // threads of a phase read 8 distinct bank quads.  Shared-memory traffic of a
 // build is then dominated by the table stores themselves.
 // ---------------------------------------------------------------------------
@@ -209,11 +209,11 @@ struct FusedShape {
     static constexpr int kRegionFloats = kCodes * 64;
     static constexpr int kPsumFloats = kRegions * kRegionFloats;
     static constexpr int kSliceSegs = 32 * U;
-    // staged x: per (u, lane quad q) a block of 2V binary16 pairs + skew
-    static constexpr int kXQW = V <= 4 ? 12 : 2 * V + 4;  // 32-bit words per block
-    static constexpr int kXWords = U * 8 * kXQW;
+    // staged x: per (u, lane quad q) a block of 2V binary32 pairs + 16-B skew
+    static constexpr int kXQF = 4 * V + 4;  // floats per block
+    static constexpr int kXFloats = U * 8 * kXQF;
     static constexpr int kPsumBytes = 4 * kPsumFloats;
-    static constexpr int kXBytes = 4 * kXWords;
+    static constexpr int kXBytes = 4 * kXFloats;
     static constexpr int kTileBytes = M * U * 512;  // codes per (slice, row group)
     static constexpr int kXPerThread = (V * kSliceSegs + kThreads - 1) / kThreads;
     static constexpr int kCPT = kCodes / (4 * kWarps) > 0 ? kCodes / (4 * kWarps) : 1;
@@ -232,15 +232,15 @@ struct FusedShape {
 #endif
 };
 
-// binary16 index (in the staged x buffer) of element k of slice segment s:
-// the pair (x_{s0,k}, x_{s1,k}) of lanes 4q+2h, 4q+2h+1 at the same u is one
-// 32-bit word, half lo.
+// float index (in the staged x buffer) of element k of slice segment s: the
+// pair (x_{s0,k}, x_{s1,k}) of lanes 4q+2h, 4q+2h+1 at the same u is one
+// 8-byte FFMA2 operand, element lo; binary32 so the build converts nothing.
 template <int V, int M, int U, int KB>
-__device__ __forceinline__ int x16_index(int s, int k) {
+__device__ __forceinline__ int x_index(int s, int k) {
     using S = FusedShape<V, M, U, KB>;
     const int l = s / U, u = s - (s / U) * U;
     const int q = l >> 2, i = l & 3, h = i >> 1, lo = i & 1;
-    return (((u * 8 + q) * S::kXQW + h * V + k) << 1) | lo;
+    return (u * 8 + q) * S::kXQF + ((h * V + k) << 1) + lo;
 }
 
 // Load this thread's share of the slice of x (column `col`), binary16.
@@ -277,23 +277,23 @@ __device__ __forceinline__ void load_x(uint16_t (&r)[FusedShape<V, M, U, KB>::kX
 }
 
 template <int V, int M, int U, int KB>
-__device__ __forceinline__ void store_x(uint16_t* x16,
+__device__ __forceinline__ void store_x(float* xs,
                                         const uint16_t (&r)[FusedShape<V, M, U, KB>::kXPerThread],
                                         int tid) {
     using S = FusedShape<V, M, U, KB>;
 #pragma unroll
     for (int i = 0; i < S::kXPerThread; ++i) {
         const int l = tid + i * kThreads;
-        if (l < S::kSliceSegs * V) x16[x16_index<V, M, U, KB>(l / V, l % V)] = r[i];
+        if (l < S::kSliceSegs * V) xs[x_index<V, M, U, KB>(l / V, l % V)] = h2f(r[i]);
     }
 }
 
 // raw binary16 x slice (TMA-staged, `valid` elements) -> staged pairs, zero past the end
 template <int V, int M, int U, int KB>
-__device__ __forceinline__ void stage_x_raw(uint16_t* x16, const uint16_t* xr, int valid, int tid) {
+__device__ __forceinline__ void stage_x_raw(float* xs, const uint16_t* xr, int valid, int tid) {
     using S = FusedShape<V, M, U, KB>;
     for (int e = tid; e < S::kSliceSegs * V; e += kThreads)
-        x16[x16_index<V, M, U, KB>(e / V, e % V)] = e < valid ? xr[e] : (uint16_t)0;
+        xs[x_index<V, M, U, KB>(e / V, e % V)] = e < valid ? h2f(xr[e]) : 0.0f;
 }
 
 // V binary16 centroid components -> binary32
@@ -337,10 +337,10 @@ __device__ __forceinline__ void psum_entries(float* dst, const float (&cc)[V],
     *reinterpret_cast<float4*>(dst) = make_float4(a01.x, a01.y, a23.x, a23.y);
 }
 
-// books16: raw binary16 codebooks [t][kcount][V];  x16: staged x pairs
+// books16: raw binary16 codebooks [t][kcount][V];  xs: staged x pairs
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ void build_psumbook_smem(float* psum, const uint16_t* books16,
-                                                    const uint32_t* x16w, int kcount, int tid) {
+                                                    const float* xs, int kcount, int tid) {
     using S = FusedShape<V, M, U, KB>;
     const int lane = tid & 31, warp = tid >> 5;
     const int q = lane & 7;      // this thread writes lanes 4q..4q+3 of a code row
@@ -366,25 +366,13 @@ __device__ __forceinline__ void build_psumbook_smem(float* psum, const uint16_t*
             // x01[k] = (x_s0k, x_s1k), x23[k] = (x_s2k, x_s3k)
             float2 x01[V], x23[V];
             {
-                const uint32_t* src = x16w + (uu * 8 + q) * S::kXQW;
-                uint32_t w[2 * V];
+                const float4* src = reinterpret_cast<const float4*>(xs + (uu * 8 + q) * S::kXQF);
 #pragma unroll
-                for (int i = 0; i < 2 * V; i += 4) {
-                    if (i + 4 <= 2 * V) {
-                        const uint4 a = *reinterpret_cast<const uint4*>(src + i);
-                        w[i] = a.x;
-                        w[i + 1] = a.y;
-                        w[i + 2] = a.z;
-                        w[i + 3] = a.w;
-                    } else {  // V == 1 never instantiated; 2V == 4 covers V == 2
-                        w[i] = src[i];
-                        w[i + 1] = src[i + 1];
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < V; ++k) {
-                    x01[k] = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
-                    x23[k] = __half22float2(*reinterpret_cast<const __half2*>(&w[V + k]));
+                for (int c = 0; c < V; ++c) {  // 2V pairs = V float4
+                    const float4 w = src[c];
+                    float2* d = (2 * c < V) ? &x01[2 * c] : &x23[2 * c - V];
+                    d[0] = make_float2(w.x, w.y);
+                    d[1] = make_float2(w.z, w.w);
                 }
             }
             float* dst = psum + (j >> 1) * S::kRegionFloats + (j & 1) * 32 + q * 4;
@@ -850,7 +838,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     const int l = c.l;
     const LayerTask& L = p.layer[l];
     float* psum = reinterpret_cast<float*>(smem_raw + p.off_psum);
-    uint16_t* x16 = reinterpret_cast<uint16_t*>(smem_raw + p.off_x);
+    float* xs = reinterpret_cast<float*>(smem_raw + p.off_x);
     const uint16_t* scl_s = reinterpret_cast<const uint16_t*>(smem_raw + p.off_scl[buf]);
     const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem_raw + p.off_raw[buf]);
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
@@ -914,15 +902,15 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
         }
         if (x_by_copy(p, L)) {
             const int64_t e0 = (int64_t)slice * (S::kSliceSegs * V);
-            stage_x_raw<V, M, U, KB>(x16, raw + p.raw_x_off / 2,
+            stage_x_raw<V, M, U, KB>(xs, raw + p.raw_x_off / 2,
                                      (int)min((int64_t)(S::kSliceSegs * V), L.cols - e0), tid);
         } else {
-            store_x<V, M, U, KB>(x16, xreg, tid);
+            store_x<V, M, U, KB>(xs, xreg, tid);
         }
         __syncthreads();
         if (col == 0) CG_STAMP(5)
         if (!(p.flags & kFlagDbgSkipBuild))
-            build_psumbook_smem<V, M, U, KB>(psum, raw, reinterpret_cast<const uint32_t*>(x16),
+            build_psumbook_smem<V, M, U, KB>(psum, raw, xs,
                                              L.kcount, tid);
         __syncthreads();
         if (col == 0) CG_STAMP(6)
@@ -1151,16 +1139,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* psum = reinterpret_cast<float*>(smem_raw + p.off_psum);
     uint16_t* books16 = reinterpret_cast<uint16_t*>(smem_raw + p.off_books);
-    uint16_t* x16 = reinterpret_cast<uint16_t*>(smem_raw + p.off_x);
+    float* xs = reinterpret_cast<float*>(smem_raw + p.off_x);
     const int tid = threadIdx.x;
     const int64_t slice = blockIdx.x;
     const int col = blockIdx.y;
     for (int e = tid; e < M * p.kcount * V; e += kThreads) books16[e] = p.books[e];
     uint16_t xreg[S::kXPerThread];
     load_x<V, M, U, KB>(xreg, p.x, slice, p.cols, p.n, col, tid);
-    store_x<V, M, U, KB>(x16, xreg, tid);
+    store_x<V, M, U, KB>(xs, xreg, tid);
     __syncthreads();
-    build_psumbook_smem<V, M, U, KB>(psum, books16, reinterpret_cast<const uint32_t*>(x16),
+    build_psumbook_smem<V, M, U, KB>(psum, books16, xs,
                                      p.kcount, tid);
     __syncthreads();
     const int total = S::kSub * p.kcount * 32;
