@@ -348,10 +348,13 @@ int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* con
     {
         const int sms = layers[0]->sms;
         bool forced = false;
+        // columns the per-task smem buffers scale with: reduce-add mode adds the
+        // partials of several columns straight into y (no staging)
+        const int n_stage = (layers[0]->flags & CG_OPT_DETERMINISTIC) ? n : 1;
         int64_t cap = 1 << 30;
         for (int i = 0; i < count; ++i) {
             forced |= layers[i]->rg_forced;
-            cap = std::min<int64_t>(cap, layers[i]->rg_cap / n);
+            cap = std::min<int64_t>(cap, layers[i]->rg_cap / n_stage);
         }
         if (!forced) {
             for (int st = 0; st < gp.n_stages; ++st) {
@@ -401,10 +404,11 @@ int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* con
     // fix-up list / owned-ticket targets (deterministic) or the staging buffer
     // of a task's partial rows (reduce-add): the larger of the two
     const int cap = rg_max * n + 16;
-    const int list_bytes = (int)list_bytes_for(rg_max, n);
+    const int n_buf = (layers[0]->flags & CG_OPT_DETERMINISTIC) ? n : 1;
+    const int list_bytes = (int)list_bytes_for(rg_max, n_buf);
     cg::SmemLayout lay;
     if (!cg::smem_layout(zmax, scl_max, raw_bytes, list_bytes, layers[0]->reserved, &lay,
-                         rg_max * 16 * n * 4))
+                         rg_max * 16 * n_buf * 4))
         return fail(CG_ERR_CONFIG,
                     "fused kernel does not fit in shared memory at n=%d (rows per task %d); "
                     "use fewer columns per call or CG_MODE_STRICT", n, rg_max);
@@ -627,8 +631,8 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
         cudaMemset(L->grid_flags, 0, fb);
     }
     if (p.fast && std::getenv("CG_STAMPS")) {
-        if ((rc = dev_alloc(L, &L->stamps, (size_t)L->sms * 512, "stamps"))) return bail(rc);
-        cudaMemset(L->stamps, 0, (size_t)L->sms * 512);
+        if ((rc = dev_alloc(L, &L->stamps, (size_t)L->sms * 1024, "stamps"))) return bail(rc);
+        cudaMemset(L->stamps, 0, (size_t)L->sms * 1024);
     }
     *out = L;
     return CG_OK;
@@ -782,7 +786,7 @@ int cg_psumbook_build(const void* books, const void* x, int m, int b, int v, int
 extern "C" int cg_debug_stamps(cg_layer* L, unsigned long long* host, int64_t count) {
     if (!L || !L->stamps) return fail(CG_ERR_ARG, "no stamps (set CG_STAMPS=1)");
     DeviceGuard guard(L->device);
-    const int64_t n = std::min<int64_t>(count, (int64_t)L->sms * 64);
+    const int64_t n = std::min<int64_t>(count, (int64_t)L->sms * 128);
     CG_CUDA(cudaMemcpy(host, L->stamps, n * 8, cudaMemcpyDeviceToHost), "stamps D2H");
     return CG_OK;
 }

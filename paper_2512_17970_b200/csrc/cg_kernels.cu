@@ -611,7 +611,7 @@ struct FixupEntry {
 // mbarrier, the fix-up count, the previous task (closed at the start of the
 // next task, after that task's input loads are in flight, or at kernel end)
 // and the zero-barrier generation.
-constexpr int kTaskList = 48;
+constexpr int kTaskList = 40;
 struct CtaState {
     uint64_t in_bar[2];           // mbarriers of the two task-input buffers
     int list_count;
@@ -624,10 +624,12 @@ struct CtaState {
     int n_bar;                    // stage barriers passed (diagnostics)
     // this CTA's task list, enumerated once at kernel start (task switches
     // must not walk the layer table: indexed parameter loads are slow)
+    int l_stage[kMaxGroup], l_tasks[kMaxGroup];  // per layer, copied from the parameters
     int n_tl;                     // entries (kTaskList = more tasks follow)
     int tl_l[kTaskList], tl_g[kTaskList];
     long long tl_t[kTaskList];
 };
+static_assert(sizeof(CtaState) <= 1024, "CtaState exceeds its shared-memory slot (kState)");
 struct PrevTask {
     int layer;
     long long slice, rg0, rg1;
@@ -741,39 +743,30 @@ struct TaskCoord {
     int64_t g;
 };
 
-// first layer index of stage s (layers are sorted by stage), n_layers if none
-__device__ __forceinline__ int stage_first(const GroupParams& p, int s) {
+// stage-wide task number g of stage s -> (l, t), false past the stage; walks
+// the shared-memory copy of the layers' {stage, n_tasks} (no dependent
+// parameter-space loads: they cost ~0.8 us per walk)
+__device__ __forceinline__ bool locate_s(const CtaState& cs, int nl, int s, int64_t g,
+                                         TaskCoord& c) {
     int l = 0;
-    while (l < p.n_layers && p.layer[l].stage < s) ++l;
-    return l;
-}
-
-// stage-wide task number g of stage s -> (l, t); false if g is past the stage
-__device__ __forceinline__ bool locate(const GroupParams& p, int s, int64_t g, TaskCoord& c) {
-    int l = stage_first(p, s);
+    while (l < nl && cs.l_stage[l] < s) ++l;
     int64_t r = g;
-    while (l < p.n_layers && p.layer[l].stage == s && r >= p.layer[l].n_tasks) {
-        r -= p.layer[l].n_tasks;
+    while (l < nl && cs.l_stage[l] == s && r >= cs.l_tasks[l]) {
+        r -= cs.l_tasks[l];
         ++l;
     }
-    if (l >= p.n_layers || p.layer[l].stage != s) return false;
+    if (l >= nl || cs.l_stage[l] != s) return false;
     c.l = l;
     c.t = r;
     c.g = g;
     return true;
 }
-
-// this CTA's first task in stage s or later
-__device__ __forceinline__ bool first_task_from(const GroupParams& p, int s, TaskCoord& c) {
-    for (; s < p.n_stages; ++s)
-        if (locate(p, s, (int64_t)blockIdx.x, c)) return true;
+__device__ __forceinline__ bool next_task_s(const CtaState& cs, int nl, int ns, TaskCoord& c) {
+    const int s = cs.l_stage[c.l];
+    if (locate_s(cs, nl, s, c.g + gridDim.x, c)) return true;
+    for (int s2 = s + 1; s2 < ns; ++s2)
+        if (locate_s(cs, nl, s2, (int64_t)blockIdx.x, c)) return true;
     return false;
-}
-
-__device__ __forceinline__ bool next_task(const GroupParams& p, TaskCoord& c) {
-    const int s = p.layer[c.l].stage;
-    if (locate(p, s, c.g + gridDim.x, c)) return true;
-    return first_task_from(p, s + 1, c);
 }
 
 __device__ __forceinline__ bool x_by_copy(const GroupParams& p, const LayerTask& L) {
@@ -843,7 +836,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem_raw + p.off_raw[buf]);
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
     unsigned long long* stamps =
-        (p.stamps && task_idx < 6) ? p.stamps + blockIdx.x * 64 + task_idx * 8 : nullptr;
+        (p.stamps && task_idx < 12) ? p.stamps + blockIdx.x * 128 + task_idx * 8 : nullptr;
 #define CG_STAMP(k) \
     if (stamps && tid == 0) stamps[k] = gtimer();
 
@@ -892,7 +885,11 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     const int gi = lg >= 5 ? 0 : (lane >> lg);
     const uint16_t* sp0 = scl_s + (warp * n_gs + gi) * 16 + sbase;
     const int sstep = kWarps * n_gs * 16;
-    const bool stage_out = split && !(p.flags & kFlagDeterministic);
+    // split-K partials: staged in smem and flushed by one bulk reduce-add per
+    // task (one column), or -- several columns -- added straight into y with
+    // red.global.add (staging would shrink tasks by the column count)
+    const bool direct = split && !(p.flags & kFlagDeterministic) && n > 1;
+    const bool stage_out = split && !(p.flags & kFlagDeterministic) && n == 1;
     const int64_t row_step = (int64_t)kWarps * 16;
 
     for (int col = 0; col < n; ++col) {
@@ -921,7 +918,13 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
                 if (d < my_rgs) load_tile<V, M, U, KB>(tb[d], cptr + d * kStep);
         }
         float* out = stage_out ? reinterpret_cast<float*>(smem_raw + p.off_stage[buf]) - rg0 * 16 * n
-                               : (split ? L.ws + (int64_t)slice * L.rows * n : L.y);
+                               : (direct ? L.y : (split ? L.ws + (int64_t)slice * L.rows * n : L.y));
+        if (direct && !cs.zero_ready) {  // y zeroed grid-wide before the first add
+            __syncthreads();
+            if (tid == 0) grid_wait(p, cs, 1);
+            __syncthreads();
+            if (tid == 0) cs.zero_ready = 1;
+        }
         int64_t row = (rg0 + warp) * 16 + mask;
         // D-deep register pipeline: tile i+D is requested as soon as tile i is consumed
         const int n_rgs = (p.flags & kFlagDbgSkipGather) ? 0 : my_rgs;
@@ -934,7 +937,10 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
                     const float v = gather_row_group<V, M, U, KB>(tb[d], sp0 + i * sstep, lb0, lb1,
                                                                   mask);
                     if (i + D < load_rgs) load_tile<V, M, U, KB>(tb[d], cptr + (i + D) * kStep);
-                    if (lane < 16 && row < L.rows) out[row * n + col] = v;
+                    if (lane < 16 && row < L.rows) {
+                        if (direct) atomicAdd(out + row * n + col, v);  // (RED, result unused)
+                        else out[row * n + col] = v;
+                    }
                     row += row_step;
                 }
             }
@@ -984,7 +990,7 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
     close_task(p, smem_raw, tid);  // deterministic split-K: pending ordered sums
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
     unsigned long long* st =
-        (p.stamps && cs.n_bar < 3) ? p.stamps + blockIdx.x * 64 + 48 + 4 * cs.n_bar : nullptr;
+        (p.stamps && cs.n_bar < 7) ? p.stamps + blockIdx.x * 128 + 96 + 4 * cs.n_bar : nullptr;
     const bool first_bar = true;  // (stamps of the first three barriers)
     if (tid == 0) {
         if (st && first_bar) st[0] = gtimer();
@@ -1017,10 +1023,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (p.flags & kFlagDbgEmpty) return;
     const int tid = threadIdx.x;
-    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 64 + 60] = gtimer();
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 124] = gtimer();
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
+    if (tid < p.n_layers) {
+        cs.l_stage[tid] = p.layer[tid].stage;
+        cs.l_tasks[tid] = p.layer[tid].n_tasks;
+    }
+    __syncthreads();
     TaskCoord c{0, 0, 0};
-    bool have = first_task_from(p, 0, c);
+    bool have = false;
+    for (int s = 0; s < p.n_stages && !have; ++s) have = locate_s(cs, p.n_layers, s, blockIdx.x, c);
     if (tid == 0) {
         mbar_init(&cs.in_bar[0], 1);
         mbar_init(&cs.in_bar[1], 1);
@@ -1041,7 +1053,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 cs.tl_t[cnt] = e.t;
                 cs.tl_g[cnt] = (int)e.g;
                 ++cnt;
-                more = next_task(p, e);
+                more = next_task_s(cs, p.n_layers, p.n_stages, e);
             }
             cs.n_tl = more ? kTaskList + 1 : cnt;  // kTaskList + 1: list full, more follow
         } else {
@@ -1050,7 +1062,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // every layer's x (and y, for write-after-read) belongs to earlier work
     pdl_wait();
-    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 64 + 62] = gtimer();
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 126] = gtimer();
     if (tid == 0) {  // (barrier state is used by thread 0 only)
         unsigned long long b;
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(b)
@@ -1060,7 +1072,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         cs.n_arrive = 0;
     }
     int stage = 0;
-    if (tid == 0 && have && p.layer[c.l].stage == 0)
+    if (tid == 0 && have && cs.l_stage[c.l] == 0)
         issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, false, true);
     if (!(p.flags & kFlagDeterministic)) {
         // zero this CTA's share of every split layer's output; each warp
@@ -1085,11 +1097,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     __syncthreads();  // CTA state (task list, mbarriers) visible to every thread
-    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 64 + 61] = gtimer();
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 125] = gtimer();
     int buf = 0, task_idx = 0;
     bool first = true;
     while (true) {
-        const int target = have ? p.layer[c.l].stage : p.n_stages - 1;
+        const int target = have ? cs.l_stage[c.l] : p.n_stages - 1;
         while (stage < target) {  // (CTAs without tasks in a stage still take part)
             stage_barrier(p, smem_raw, tid);
             ++stage;
@@ -1107,9 +1119,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else if (cs.n_tl <= kTaskList && task_idx + 1 >= cs.n_tl) {
             has_next = false;
         } else {
-            has_next = next_task(p, nc);  // beyond the enumerated list (rare)
+            has_next = next_task_s(cs, p.n_layers, p.n_stages, nc);  // beyond the list (rare)
         }
-        const bool x_next = has_next && p.layer[nc.l].stage == stage;
+        const bool x_next = has_next && cs.l_stage[nc.l] == stage;
         run_task<V, M, U, KB>(p, c, buf, first, has_next, x_next, nc, smem_raw, tid, task_idx++);
         first = false;
         buf ^= 1;
@@ -1127,7 +1139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      : "memory");
     }
     __syncthreads();
-    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 64 + 63] = gtimer();
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 127] = gtimer();
 }
 
 // dump the fused kernel's smem Psumbook in _psum_tables layout (m, segs, 2**b, n):
