@@ -622,6 +622,7 @@ struct CtaState {
     int prev_layer;
     long long prev_slice, prev_rg0, prev_rg1;
     int n_bar;                    // stage barriers passed (diagnostics)
+    int zero_pending;             // this CTA's zeroing arrival (grid barrier 1) not made yet
     // this CTA's task list, enumerated once at kernel start (task switches
     // must not walk the layer table: indexed parameter loads are slow)
     int l_stage[kMaxGroup], l_tasks[kMaxGroup];  // per layer, copied from the parameters
@@ -659,6 +660,14 @@ __device__ __forceinline__ void grid_wait(const GroupParams& p, const CtaState& 
         if (f >= want) break;
         __nanosleep(32);
     }
+}
+
+// The zeroing arrival (grid barrier 1): every thread's zero stores are
+// fenced (cheap by now), then one reduction per warp.
+__device__ __forceinline__ void zero_arrive(const GroupParams& p, int tid) {
+    __threadfence();
+    __syncwarp();
+    if ((tid & 31) == 0) grid_red(p, 1);
 }
 
 // Split-K close of a task.  Every (row group, column) of the task takes a
@@ -825,7 +834,8 @@ __device__ __forceinline__ void issue_inputs(const GroupParams& p, TaskCoord c, 
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int buf, bool first_task,
                                          bool has_next, bool x_next, TaskCoord nc,
-                                         unsigned char* smem_raw, int tid, int task_idx) {
+                                         unsigned char* smem_raw, int tid, int task_idx,
+                                         bool zero_todo) {
     using S = FusedShape<V, M, U, KB>;
     constexpr int D = S::kDepth;
     const int l = c.l;
@@ -912,6 +922,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
         __syncthreads();
         if (col == 0) CG_STAMP(6)
         if (col == 0 && first_task) pdl_launch_dependents();
+        if (col == 0 && zero_todo) zero_arrive(p, tid);
         if (col > 0) {
 #pragma unroll
             for (int d = 0; d < D; ++d)
@@ -1041,6 +1052,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         cs.zero_ready = 0;
         cs.prev_layer = -1;
         cs.n_bar = 0;
+        cs.zero_pending = 0;
+        cs.n_arrive = 0;
         // weights of the first task (and its code range into L2) travel
         // before the wait on the previous kernel
         if (have) issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, true, false);
@@ -1063,24 +1076,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     // every layer's x (and y, for write-after-read) belongs to earlier work
     pdl_wait();
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 126] = gtimer();
-    if (tid == 0) {  // (barrier state is used by thread 0 only)
+    int stage = 0;
+    if (tid == 0 && have && cs.l_stage[c.l] == 0)
+        issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, false, true);
+    if (tid == 32) {  // barrier state (used by thread 0 after the prologue barrier)
         unsigned long long b;
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(b)
                      : "l"(p.grid_flags + 16 + blockIdx.x)
                      : "memory");
         cs.bar_base = b;
-        cs.n_arrive = 0;
     }
-    int stage = 0;
-    if (tid == 0 && have && cs.l_stage[c.l] == 0)
-        issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, false, true);
     if (!(p.flags & kFlagDeterministic)) {
         // zero this CTA's share of every split layer's output; each warp
         // releases its own stores (arrival 1: one unit per warp), so no CTA
         // barrier sits on this path -- the first flush waits for the grid
+        // (static layer indices: parameter loads with immediate offsets)
         bool any = false;
-        const int warp = tid >> 5, lane = tid & 31;
-        for (int l = 0; l < p.n_layers; ++l) {
+#pragma unroll
+        for (int l = 0; l < kMaxGroup; ++l) {
+            if (l >= p.n_layers) break;
             const LayerTask& L = p.layer[l];
             if (L.n_slices <= 1) continue;
             any = true;
@@ -1089,20 +1103,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t e0 = blockIdx.x * per, e1 = min(e0 + per, elems);
             for (int64_t e = e0 + tid; e < e1; e += kThreads) L.y[e] = 0.0f;
         }
-        if (any) {
-            __syncwarp();
-            if (lane == 0) grid_red(p, 1);  // release: orders the warp's zero stores
-            if (tid == 0) cs.n_arrive = 1;
-            (void)warp;
+        // the arrival (fenced) is made after the CTA's first Psumbook build,
+        // when these stores have long completed -- off the prologue's path
+        if (any && tid == 0) {
+            cs.n_arrive = 1;
+            cs.zero_pending = 1;
         }
     }
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 122] = gtimer();
     __syncthreads();  // CTA state (task list, mbarriers) visible to every thread
+    bool zero_todo = cs.zero_pending != 0;  // (same in every thread)
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 125] = gtimer();
     int buf = 0, task_idx = 0;
     bool first = true;
     while (true) {
         const int target = have ? cs.l_stage[c.l] : p.n_stages - 1;
         while (stage < target) {  // (CTAs without tasks in a stage still take part)
+            if (zero_todo) {  // the zeroing arrival precedes every stage arrival
+                zero_arrive(p, tid);
+                zero_todo = false;
+            }
             stage_barrier(p, smem_raw, tid);
             ++stage;
             if (tid == 0 && have && stage == target)
@@ -1122,12 +1142,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             has_next = next_task_s(cs, p.n_layers, p.n_stages, nc);  // beyond the list (rare)
         }
         const bool x_next = has_next && cs.l_stage[nc.l] == stage;
-        run_task<V, M, U, KB>(p, c, buf, first, has_next, x_next, nc, smem_raw, tid, task_idx++);
+        run_task<V, M, U, KB>(p, c, buf, first, has_next, x_next, nc, smem_raw, tid, task_idx++,
+                              zero_todo);
+        zero_todo = false;
         first = false;
         buf ^= 1;
         c = nc;
         have = has_next;
     }
+    if (zero_todo) zero_arrive(p, tid);  // (a CTA without any task)
     // close the last task's row groups; drain the bulk reduce-adds
     __syncthreads();
     close_task(p, smem_raw, tid);

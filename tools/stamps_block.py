@@ -74,6 +74,7 @@ def show(name, col):
 
 show("kernel entry", st[:, 124])
 show("pdl_wait passed", st[:, 126])
+show("zeroing done (tid 0)", st[:, 122])
 show("prologue done", st[:, 125])
 names = [(0, "start"), (7, "synced"), (4, "inputs ok"), (5, "x staged"), (6, "table ready"),
          (1, "gathered"), (2, "zero ok/flush"), (3, "task end")]
