@@ -364,3 +364,34 @@ def test_staged_launch_rejects_mixed_tiling_and_bad_stages():
         cg.gemm_stages([a, b], [x, x], ys, [0, 1])
     with pytest.raises(ValueError):
         cg.gemm_stages([a, a], [x, x], ys, [0, 2])
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_multi_column_direct_add_vs_c_oracle(n):
+    """n > 1 in reduce-add mode adds split-K partials straight into y (red.add)."""
+    q = cg.random_layer(3000, 4096, cg.QuantConfig(v=4, m=1, b=8, g=128), seed=60 + n)
+    x16 = orc.bench_input_array(4096, n, n)
+    ref = c_oracle.codegemm([p.codes for p in q.planes], [b.entries for b in q.books],
+                            q.scales.scales, x16, 4, 128, threads=8)
+    for u in (2, 4):
+        dl = cg.DeviceLayer(q, u=u)
+        for _ in range(2):
+            assert_within_tolerance(dl.gemm(cuda_x(x16)).cpu().numpy(), ref, f"n={n} u={u}")
+
+
+def test_staged_chain_m2v8():
+    """The second 2-bit configuration (m2v8g128) through a dependent staged chain."""
+    cfg = cg.QuantConfig(v=8, m=2, b=8, g=128)
+    shapes = [(2048, 1024), (1024, 2048), (3072, 1024)]
+    qs = [cg.random_layer(r, c, cfg, seed=700 + i) for i, (r, c) in enumerate(shapes)]
+    layers = [cg.DeviceLayer(q, u=1) for q in qs]
+    x0 = orc.bench_input_array(1024, 1, 4)
+    ys = [torch.empty((r, 1), dtype=torch.float32, device="cuda") for r, _ in shapes]
+    cg.gemm_stages(layers, [cuda_x(x0), ys[0], ys[1]], ys, [0, 1, 2])
+    got = [y.cpu().numpy() for y in ys]
+    xin = x0
+    for i, q in enumerate(qs):
+        ref = c_oracle.codegemm([p.codes for p in q.planes], [b.entries for b in q.books],
+                                q.scales.scales, xin, 8, 128, threads=8)
+        assert_within_tolerance(got[i], ref, f"m2v8 stage {i}")
+        xin = got[i].astype(np.float16)
