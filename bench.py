@@ -72,7 +72,7 @@ STEP_GROUPS = ((0, 1, 2), (3,), (4, 5), (6,))
 # the staged step (N=1): stage of each layer and the layer whose y it reads
 STEP_STAGES = (0, 0, 0, 1, 2, 2, 3)
 STEP_XSRC = (None, None, None, 0, 3, 3, 4)
-TILING_U = 2  # one tiling for every layer of a staged launch (64 KB Psumbooks)
+TILING_U = int(os.environ.get("CG_BENCH_U", "0"))  # one tiling for every layer of a staged launch (0: 4 // m)
 
 
 def block_spec(workload: str):
@@ -263,6 +263,9 @@ def main():
         args.workload = "8b" if world == 1 else "70b"
     cfg = CONFIGS[args.config]
     n = args.batch
+    global TILING_U
+    if TILING_U == 0:
+        TILING_U = 4 // cfg["m"]  # measured: u=4 41.5 us/block vs u=2 43.6 vs u=1 57.4 (m1v4)
     spec = block_spec(args.workload)
     if args.warmup < 3:
         args.warmup = 3

@@ -25,7 +25,7 @@ spec = bench.block_spec("8b")
 nl = len(spec)
 sets = []
 for k in range(2):
-    layers = [cg.DeviceLayer(bench.make_layer(r, c, cfg, 100 * k + 7 * j + i), u=bench.TILING_U)
+    layers = [cg.DeviceLayer(bench.make_layer(r, c, cfg, 100 * k + 7 * j + i), u=bench.TILING_U or 4)
               for j in range(chain) for i, (_, r, c) in enumerate(spec)]
     ys = [torch.empty((r, 1), dtype=torch.float32, device="cuda") for j in range(chain)
           for (_, r, c) in spec]
