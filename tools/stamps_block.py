@@ -80,7 +80,7 @@ names = [(0, "start"), (7, "synced"), (4, "inputs ok"), (5, "x staged"), (6, "ta
          (1, "gathered"), (2, "zero ok/flush"), (3, "task end")]
 for k in range(12):
     for slot, nm in names:
-        if slot in (0, 6, 1, 3):
+        if slot in (0, 7, 4, 5, 6, 1, 3):
             show(f"task{k} {nm}", st[:, k * 8 + slot])
 for b in range(7):
     for j, nm in enumerate(("entered", "drained", "arrived", "released")):
