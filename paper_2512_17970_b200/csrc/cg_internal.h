@@ -39,6 +39,9 @@ struct LayerTask {
     int64_t rows, cols, n_rg, n_slices, n_rb;
     int u, rg_per_task, lg, n_gs, kcount, n_tasks;
     int stage;                // dependency stage within the launch (non-decreasing)
+    int dep;                  // layer whose y this layer's x is (row-group readiness), or -1
+    unsigned long long* rg_cnt;  // [0] launches completed, [1 + rg] row-group completions
+                                 // (this layer is a producer for a later layer), or null
 };
 
 constexpr int kMaxGroup = 16;
@@ -78,6 +81,7 @@ constexpr int kFlagLastArriver = 4;  // a layer has more tasks than the grid: la
 constexpr int kFlagDeterministic = 16;  // split-K by tickets + ordered sums (else L2 reduce-add)
 constexpr int kFlagXRegs = 32;  // x staged through registers (unaligned x / odd cols / n > 1)
 // diagnostics only (CG_DEBUG_FLAGS): wrong results, phase isolation for timing
+constexpr int kFlagRowDeps = 64;  // stages ordered by row-group readiness, not grid barriers
 constexpr int kFlagDbgSkipBuild = 1 << 8;   // no Psumbook build
 constexpr int kFlagDbgNoLoads = 1 << 9;     // gather reuses the preloaded code tiles
 constexpr int kFlagDbgSkipGather = 1 << 10; // no gather

@@ -485,9 +485,6 @@ __device__ __forceinline__ void bulk_reduce_add_f32(float* dst, const float* src
         : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
 // all but the most recent bulk group have finished reading shared memory
 __device__ __forceinline__ void bulk_wait_read_prev() {
     asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -623,9 +620,12 @@ struct CtaState {
     long long prev_slice, prev_rg0, prev_rg1;
     int n_bar;                    // stage barriers passed (diagnostics)
     int zero_pending;             // this CTA's zeroing arrival (grid barrier 1) not made yet
+    int sig_layer;                // row deps: producer task whose completion is still to signal
+    long long sig_rg0, sig_rg1;
     // this CTA's task list, enumerated once at kernel start (task switches
     // must not walk the layer table: indexed parameter loads are slow)
     int l_stage[kMaxGroup], l_tasks[kMaxGroup];  // per layer, copied from the parameters
+    unsigned long long l_gen[kMaxGroup];  // producer layers: completed launches (row deps)
     int n_tl;                     // entries (kTaskList = more tasks follow)
     int tl_l[kTaskList], tl_g[kTaskList];
     long long tl_t[kTaskList];
@@ -668,6 +668,41 @@ __device__ __forceinline__ void zero_arrive(const GroupParams& p, int tid) {
     __threadfence();
     __syncwarp();
     if ((tid & 31) == 0) grid_red(p, 1);
+}
+
+// ---- row-group readiness (kFlagRowDeps) ----
+// A producer layer's counter rg_cnt[1 + rg] gains one per slice task covering
+// row group rg once that task's contribution to y is complete (bulk
+// reduce-adds drained, or plain stores) and released; rg_cnt[0] counts the
+// launches that completed, so in this launch the row group is final at
+// (gen + 1) * n_slices.  A consumer task waits (one warp) for the row groups
+// of the producer's y that its x slice reads.
+__device__ __forceinline__ void wait_rows(const unsigned long long* cnt, unsigned long long want,
+                                          int64_t rg0, int64_t rg1, int lane) {
+    for (int64_t rg = rg0 + lane; rg < rg1; rg += 32) {
+        unsigned long long f;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(cnt + 1 + rg)
+                         : "memory");
+            if (f >= want) break;
+            __nanosleep(32);
+        }
+    }
+    __syncwarp();
+}
+
+// Signal the previous producer task's row groups (thread 0): its bulk
+// reduce-adds are drained first and the async-proxy writes fenced; one
+// release fence then orders everything before the relaxed increments.
+__device__ __forceinline__ void signal_rows(const GroupParams& p, CtaState& cs) {
+    if (cs.sig_layer < 0) return;
+    const LayerTask& L = p.layer[cs.sig_layer];
+    bulk_wait_all();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // one release for all the row groups
+    for (long long rg = cs.sig_rg0; rg < cs.sig_rg1; ++rg)
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(L.rg_cnt + 1 + rg) : "memory");
+    cs.sig_layer = -1;
 }
 
 // Split-K close of a task.  Every (row group, column) of the task takes a
@@ -870,6 +905,18 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
 #pragma unroll
     for (int d = 0; d < D; ++d)
         if (d < my_rgs) load_tile<V, M, U, KB>(tb[d], cptr + d * kStep);
+    if (tid == 0) signal_rows(p, cs);  // the previous task, if a producer
+    if (L.dep >= 0) {
+        // x is an earlier stage's y: wait for the row groups this slice reads
+        if (warp == 0) {
+            const LayerTask& P = p.layer[L.dep];
+            const int64_t e0 = (int64_t)slice * (S::kSliceSegs * V);
+            const int64_t e1 = min(e0 + (int64_t)(S::kSliceSegs * V), L.cols);
+            wait_rows(P.rg_cnt, (cs.l_gen[L.dep] + 1) * (unsigned long long)P.n_slices, e0 >> 4,
+                      (e1 + 15) >> 4, lane);
+        }
+        __syncthreads();
+    }
     uint16_t xreg[S::kXPerThread];
     if (!x_by_copy(p, L)) load_x<V, M, U, KB>(xreg, L, slice, n, 0, tid);
 
@@ -981,6 +1028,11 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     }
     __syncthreads();
     if (tid == 0) {
+        if (L.rg_cnt) {  // a later stage reads this y: signal at the next task start
+            cs.sig_layer = l;
+            cs.sig_rg0 = rg0;
+            cs.sig_rg1 = rg1;
+        }
         cs.in_phase ^= (1u << buf);
         cs.prev_layer = (split && (p.flags & kFlagDeterministic)) ? l : -1;
         cs.prev_slice = slice;
@@ -1054,6 +1106,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         cs.n_bar = 0;
         cs.zero_pending = 0;
         cs.n_arrive = 0;
+        cs.sig_layer = -1;
         // weights of the first task (and its code range into L2) travel
         // before the wait on the previous kernel
         if (have) issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, true, false);
@@ -1079,6 +1132,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     if (tid == 0 && have && cs.l_stage[c.l] == 0)
         issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, false, true);
+    if (tid < p.n_layers && p.layer[tid].rg_cnt) {  // producer generations (row deps)
+        unsigned long long gv;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(gv) : "l"(p.layer[tid].rg_cnt)
+                     : "memory");
+        cs.l_gen[tid] = gv;
+    }
     if (tid == 32) {  // barrier state (used by thread 0 after the prologue barrier)
         unsigned long long b;
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(b)
@@ -1105,7 +1164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // the arrival (fenced) is made after the CTA's first Psumbook build,
         // when these stores have long completed -- off the prologue's path
-        if (any && tid == 0) {
+        if ((any || (p.flags & kFlagRowDeps)) && tid == 0) {
             cs.n_arrive = 1;
             cs.zero_pending = 1;
         }
@@ -1123,7 +1182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 zero_arrive(p, tid);
                 zero_todo = false;
             }
-            stage_barrier(p, smem_raw, tid);
+            if (!(p.flags & kFlagRowDeps)) stage_barrier(p, smem_raw, tid);
             ++stage;
             if (tid == 0 && have && stage == target)
                 issue_inputs<V, M, U, KB>(p, c, buf, smem_raw, false, true);
@@ -1156,6 +1215,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     close_task(p, smem_raw, tid);
     if (tid == 0) {
         bulk_wait_all();
+        signal_rows(p, cs);
+        if ((p.flags & kFlagRowDeps) && blockIdx.x == 0) {
+            // every CTA read the generations before its arrival 1
+            grid_wait(p, cs, 1);
+            for (int l = 0; l < p.n_layers; ++l)
+                if (p.layer[l].rg_cnt)
+                    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.layer[l].rg_cnt),
+                                 "l"(cs.l_gen[l] + 1ull)
+                                 : "memory");
+        }
         // this CTA's arrival count for the next launch on these flags
         asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.grid_flags + 16 + blockIdx.x),
                      "l"(cs.bar_base + (unsigned long long)kBarUnits * cs.n_arrive)
