@@ -82,6 +82,7 @@ constexpr int kFlagDeterministic = 16;  // split-K by tickets + ordered sums (el
 constexpr int kFlagXRegs = 32;  // x staged through registers (unaligned x / odd cols / n > 1)
 // diagnostics only (CG_DEBUG_FLAGS): wrong results, phase isolation for timing
 constexpr int kFlagRowDeps = 64;  // stages ordered by row-group readiness, not grid barriers
+constexpr int kFlagDirectAdd = 1 << 14;  // split-K partials red.add'ed into y even at n == 1
 constexpr int kFlagDbgSkipBuild = 1 << 8;   // no Psumbook build
 constexpr int kFlagDbgNoLoads = 1 << 9;     // gather reuses the preloaded code tiles
 constexpr int kFlagDbgSkipGather = 1 << 10; // no gather

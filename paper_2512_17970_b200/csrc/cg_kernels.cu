@@ -945,8 +945,9 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     // split-K partials: staged in smem and flushed by one bulk reduce-add per
     // task (one column), or -- several columns -- added straight into y with
     // red.global.add (staging would shrink tasks by the column count)
-    const bool direct = split && !(p.flags & kFlagDeterministic) && n > 1;
-    const bool stage_out = split && !(p.flags & kFlagDeterministic) && n == 1;
+    const bool direct = split && !(p.flags & kFlagDeterministic) &&
+                        (n > 1 || (p.flags & kFlagDirectAdd));
+    const bool stage_out = split && !(p.flags & kFlagDeterministic) && !direct;
     const int64_t row_step = (int64_t)kWarps * 16;
 
     for (int col = 0; col < n; ++col) {
