@@ -189,7 +189,7 @@ struct cg_layer {
     uint16_t* x_pin = nullptr;
     float* y_pin = nullptr;
     int flags = 0;
-    int pf_dist = 0;
+    int pf_dist = 2;  // L2 prefetch window in rounds of row groups (measured best: 2)
     int sms = 148;
     bool rg_forced = false;  // rg_per_task given at creation: launches keep the task split
     int rg_cap = 0;          // largest rows-per-task whose task buffers fit shared memory (n=1)
@@ -302,6 +302,7 @@ int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* con
     gp.n = n;
     gp.flags = (layers[0]->flags & CG_OPT_NO_L2_PREFETCH) ? cg::kFlagNoPrefetch : 0;
     gp.pf_dist = layers[0]->pf_dist;
+    if (const char* e = std::getenv("CG_PF_DIST")) gp.pf_dist = std::atoi(e);  // tuning knob
     gp.stamps = layers[0]->stamps;
     cg::FusedSizes zmax{0, 0, 0};
     int scl_max = 0, rg_max = 0, grid = 1, raw_bytes = 0, books_raw = 0;

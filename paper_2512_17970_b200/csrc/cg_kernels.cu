@@ -857,7 +857,11 @@ __device__ __forceinline__ void issue_inputs(const GroupParams& p, TaskCoord c, 
         if (!(p.flags & kFlagNoPrefetch)) {
             const uint8_t* base =
                 L.codes + ((int64_t)g.slice * L.n_rg + g.rg0) * (int64_t)S::kTileBytes;
-            const int64_t bytes = (g.rg1 - g.rg0) * (int64_t)S::kTileBytes;
+            // the whole range, or (pf_dist > 0) the first pf_dist rounds of row
+            // groups; the gather then keeps pf_dist rounds ahead (rolling window)
+            int64_t bytes = (g.rg1 - g.rg0) * (int64_t)S::kTileBytes;
+            if (p.pf_dist > 0)
+                bytes = min(bytes, (int64_t)p.pf_dist * kWarps * (int64_t)S::kTileBytes);
             constexpr int64_t kChunk = 32 * 1024;
             for (int64_t o = 0; o < bytes; o += kChunk)
                 prefetch_l2_bulk(base + o, (uint32_t)min(kChunk, bytes - o));
@@ -987,12 +991,15 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
         int64_t row = (rg0 + warp) * 16 + mask;
         // D-deep register pipeline: tile i+D is requested as soon as tile i is consumed
         const int n_rgs = (p.flags & kFlagDbgSkipGather) ? 0 : my_rgs;
+        const int pf = (p.flags & kFlagNoPrefetch) ? 0 : p.pf_dist;
         const int load_rgs = (p.flags & kFlagDbgNoLoads) ? 0 : my_rgs;
         for (int i0 = 0; i0 < n_rgs; i0 += D) {
 #pragma unroll
             for (int d = 0; d < D; ++d) {
                 const int i = i0 + d;
                 if (i < n_rgs) {
+                    if (pf > 0 && lane == 0 && i + pf < load_rgs)
+                        prefetch_l2_bulk(cptr - lane * 16 + (i + pf) * kStep, S::kTileBytes);
                     const float v = gather_row_group<V, M, U, KB>(tb[d], sp0 + i * sstep, lb0, lb1,
                                                                   mask);
                     if (i + D < load_rgs) load_tile<V, M, U, KB>(tb[d], cptr + (i + D) * kStep);
