@@ -103,3 +103,27 @@ def test_matrix_container():
     assert not m.data.flags.writeable
     with pytest.raises(cg.ShapeError):
         cg.Matrix(np.zeros((2, 2), np.float32))
+
+
+def test_gemm_stages_argument_checks():
+    """gemm_stages validates shapes and dtypes before touching the library."""
+    torch = pytest.importorskip("torch")
+
+    class FakeLayer:  # the attributes gemm_stages reads before the launch
+        def __init__(self, rows, cols):
+            self.rows, self.cols = rows, cols
+
+    a, b = FakeLayer(64, 128), FakeLayer(32, 64)
+    x = torch.zeros((128, 1), dtype=torch.float16)
+    ya = torch.zeros((64, 1), dtype=torch.float32)
+    yb = torch.zeros((32, 1), dtype=torch.float32)
+    with pytest.raises(cg.ShapeError):  # one x/y/stage per layer
+        cg.gemm_stages([a, b], [x], [ya, yb], [0, 1])
+    with pytest.raises(cg.ShapeError):  # x rows must be the layer's cols
+        cg.gemm_stages([a, b], [x, x], [ya, yb], [0, 1])
+    with pytest.raises(cg.ShapeError):  # x must be float16 or float32
+        cg.gemm_stages([a], [x.to(torch.float64)], [ya], [0])
+    with pytest.raises(cg.ShapeError):  # y must be (rows, n) float32
+        cg.gemm_stages([a], [x], [ya.to(torch.float16)], [0])
+    with pytest.raises(cg.ShapeError):
+        cg.gemm_stages([a], [x], [yb], [0])
