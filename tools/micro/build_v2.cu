@@ -10,20 +10,18 @@ template <int V, int M, int U, int KB>
 __device__ __forceinline__ void build_v1(float* psum, const uint16_t* books16, const float* xs,
                                          int kcount, int tid) {
     using S = FusedShape<V, M, U, KB>;
-    constexpr int kHalfW = kWarps / 2;
-    constexpr int kCP = S::kCodes / (4 * kHalfW);  // codes per thread (8 at 256 codes)
     const int lane = tid & 31, warp = tid >> 5;
-    const int half = warp / kHalfW, hw = warp - half * kHalfW;
     const int q = lane & 7, csub = lane >> 3;
-    const int c0 = csub + 4 * hw;
+    const int c0 = csub + 4 * warp;
+    constexpr int kCPT = S::kCPT;
 #pragma unroll 1
     for (int t = 0; t < M; ++t) {
         const uint16_t* bk = books16 + t * kcount * V;
-        float cc[kCP][V];
+        float cc[kCPT][V];
 #pragma unroll
-        for (int i = 0; i < kCP; ++i) load_centroid<V>(cc[i], bk + (c0 + 4 * kHalfW * i) * V);
-#pragma unroll 1
-        for (int uu = half; uu < U; uu += 2) {
+        for (int i = 0; i < kCPT; ++i) load_centroid<V>(cc[i], bk + (c0 + 4 * kWarps * i) * V);
+#pragma unroll 2
+        for (int uu = 0; uu < U; ++uu) {
             const int j = t * U + uu;
             float2 x01[V], x23[V];
             const float4* src = reinterpret_cast<const float4*>(xs + (uu * 8 + q) * S::kXQF);
@@ -36,7 +34,7 @@ __device__ __forceinline__ void build_v1(float* psum, const uint16_t* books16, c
             }
             float* dst = psum + (j >> 1) * S::kRegionFloats + (j & 1) * 32 + q * 4;
 #pragma unroll
-            for (int i = 0; i < kCP; ++i) psum_entries<V>(dst + (c0 + 4 * kHalfW * i) * 64, cc[i], x01, x23);
+            for (int i = 0; i < kCPT; ++i) psum_entries<V>(dst + (c0 + 4 * kWarps * i) * 64, cc[i], x01, x23);
         }
     }
 }
