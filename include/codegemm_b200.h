@@ -115,6 +115,15 @@ int cg_device_count(void);
 int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
                     const uint16_t* scales, int64_t rows, int64_t cols, int v, int m, int b,
                     int64_t g, const cg_layer_options* opts, cg_layer** out);
+/*
+ * The same from the CGMM container's code planes as stored (storage.py:95-160,
+ * quantizer.py:471-497): planes[t] holds rows*(cols/v) codes of b bits each,
+ * least-significant bit first, padded to a whole byte.  The planes cross PCIe
+ * at b bits per code and are unpacked and prepacked on the device.
+ */
+int cg_layer_create_packed(const uint8_t* const* planes, const uint16_t* const* books,
+                           const uint16_t* scales, int64_t rows, int64_t cols, int v, int m,
+                           int b, int64_t g, const cg_layer_options* opts, cg_layer** out);
 int cg_layer_destroy(cg_layer* layer);
 int cg_layer_query(const cg_layer* layer, cg_layer_info* info);
 

@@ -41,6 +41,7 @@ from .quantizer import (
     random_layer,
     unpack_codes,
 )
+from .storage import deserialize, load_device_layer, serialize
 from .tensors import Matrix, encode_f16_array
 
 __version__ = "0.1.0"
@@ -50,6 +51,7 @@ __all__ = [
     "DeviceLayer", "DimOverflowError", "FormatError", "IntegrityError", "Matrix", "OpCounters",
     "Psumbook", "QuantConfig", "QuantizedLayer", "ScalePlane", "ShapeError", "TileConfig",
     "TruncatedFileError", "UnsupportedVersionError", "build_psumbook", "closed_form_counters",
+    "deserialize", "load_device_layer", "serialize",
     "codegemm_gemm", "encode_f16_array", "gemm_group", "gemm_stages", "pack_codes", "phase_split", "random_layer",
     "unpack_codes",
 ]

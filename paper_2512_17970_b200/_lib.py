@@ -39,6 +39,7 @@ EXPORTS = (
     "cg_last_error",
     "cg_device_count",
     "cg_layer_create",
+    "cg_layer_create_packed",
     "cg_layer_destroy",
     "cg_layer_query",
     "cg_gemm_stages",
@@ -105,6 +106,9 @@ def load() -> ctypes.CDLL:
     lib.cg_layer_create.argtypes = [u16pp, u16pp, p, i64, i64, i, i, i, i64,
                                     ctypes.POINTER(LayerOptions), ctypes.POINTER(vp)]
     lib.cg_layer_create.restype = i
+    lib.cg_layer_create_packed.argtypes = [u16pp, u16pp, p, i64, i64, i, i, i, i64,
+                                    ctypes.POINTER(LayerOptions), ctypes.POINTER(vp)]
+    lib.cg_layer_create_packed.restype = i
     lib.cg_layer_destroy.argtypes = [vp]
     lib.cg_layer_destroy.restype = i
     lib.cg_layer_query.argtypes = [vp, ctypes.POINTER(LayerInfo)]

@@ -532,12 +532,17 @@ int cg_device_count(void) {
     return n;
 }
 
-int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
-                    const uint16_t* scales, int64_t rows, int64_t cols, int v, int m, int b,
-                    int64_t g, const cg_layer_options* opts, cg_layer** out) {
+}  // extern "C"
+
+namespace {
+// codes: uint16 planes (host), or packed: b-bit packed planes (host, CGMM layout)
+int create_layer(const uint16_t* const* codes, const uint8_t* const* packed,
+                 const uint16_t* const* books, const uint16_t* scales, int64_t rows, int64_t cols,
+                 int v, int m, int b, int64_t g, const cg_layer_options* opts, cg_layer** out) {
     if (!out) return fail(CG_ERR_ARG, "out is NULL");
     *out = nullptr;
-    if (!codes || !books || !scales) return fail(CG_ERR_ARG, "NULL codes/books/scales");
+    if ((!codes && !packed) || !books || !scales)
+        return fail(CG_ERR_ARG, "NULL codes/books/scales");
     // QuantConfig.__post_init__ / validate_shape (quantizer.py:55-84)
     if (v < 1) return fail(CG_ERR_CONFIG, "v must be >= 1, got %d", v);
     if (m < 1) return fail(CG_ERR_CONFIG, "m must be >= 1, got %d", m);
@@ -556,7 +561,8 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
         return fail(CG_ERR_CONFIG, "cols=%lld not divisible by g=%lld", (long long)cols,
                     (long long)g);
     for (int t = 0; t < m; ++t)
-        if (!codes[t] || !books[t]) return fail(CG_ERR_ARG, "NULL plane/book %d", t);
+        if (!(codes ? (const void*)codes[t] : (const void*)packed[t]) || !books[t])
+            return fail(CG_ERR_ARG, "NULL plane/book %d", t);
 
     int device = 0;
     if (opts && opts->device >= 0) device = opts->device;
@@ -631,9 +637,25 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
     e = cudaMalloc(&bad, sizeof(unsigned));
     if (e != cudaSuccess) return bail(cuda_fail(e, "flag alloc"));
     cudaMemset(bad, 0, sizeof(unsigned));
-    for (int t = 0; t < m; ++t) {
-        e = cudaMemcpy(raw + t * plane_elems, codes[t], plane_elems * 2, cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) return bail(cuda_fail(e, "plane upload"));
+    if (codes) {
+        for (int t = 0; t < m; ++t) {
+            e = cudaMemcpy(raw + t * plane_elems, codes[t], plane_elems * 2, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) return bail(cuda_fail(e, "plane upload"));
+        }
+    } else {
+        // b bits per code on the wire; unpacked to uint16 planes on the device
+        const int64_t plane_bytes = ((int64_t)plane_elems * b + 7) / 8;
+        uint8_t* pk = nullptr;
+        e = cudaMalloc(&pk, (size_t)(plane_bytes * m + 16));
+        if (e != cudaSuccess) return bail(cuda_fail(e, "packed plane staging alloc"));
+        for (int t = 0; t < m && e == cudaSuccess; ++t)
+            e = cudaMemcpy(pk + t * plane_bytes, packed[t], (size_t)plane_bytes,
+                           cudaMemcpyHostToDevice);
+        if (e == cudaSuccess)
+            e = cg::launch_unpack_packed(pk, plane_bytes, m, (int64_t)plane_elems, b, raw, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(pk);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "packed plane upload"));
     }
     if (p.fast) {
         if ((rc = dev_alloc(L, &L->codes, (size_t)p.code_bytes, "code stream alloc")))
@@ -678,6 +700,24 @@ int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
     }
     *out = L;
     return CG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cg_layer_create(const uint16_t* const* codes, const uint16_t* const* books,
+                    const uint16_t* scales, int64_t rows, int64_t cols, int v, int m, int b,
+                    int64_t g, const cg_layer_options* opts, cg_layer** out) {
+    if (!codes) return fail(CG_ERR_ARG, "NULL codes");
+    return create_layer(codes, nullptr, books, scales, rows, cols, v, m, b, g, opts, out);
+}
+
+int cg_layer_create_packed(const uint8_t* const* planes, const uint16_t* const* books,
+                           const uint16_t* scales, int64_t rows, int64_t cols, int v, int m,
+                           int b, int64_t g, const cg_layer_options* opts, cg_layer** out) {
+    if (!planes) return fail(CG_ERR_ARG, "NULL planes");
+    return create_layer(nullptr, planes, books, scales, rows, cols, v, m, b, g, opts, out);
 }
 
 int cg_layer_destroy(cg_layer* layer) {

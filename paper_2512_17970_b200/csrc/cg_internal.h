@@ -191,6 +191,8 @@ cudaError_t launch_psumbook_dump(const Plan& p, const DumpParams& dp, float* out
 cudaError_t launch_strict_gemm(const Plan& p, const uint8_t* packed, const uint16_t* raw16,
                                const uint16_t* books, const uint16_t* scales, const uint16_t* x,
                                int n, float* y, cudaStream_t s);
+cudaError_t launch_unpack_packed(const uint8_t* packed, int64_t plane_bytes, int m,
+                                 int64_t per_plane, int b, uint16_t* out, cudaStream_t s);
 cudaError_t launch_psumbook_build(const uint16_t* books, const uint16_t* x, int m, int b, int v,
                                   int64_t k_len, int n, float* out, cudaStream_t s);
 

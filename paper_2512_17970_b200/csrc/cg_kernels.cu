@@ -175,6 +175,29 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed,
     }
 }
 
+// CGMM code planes as stored (quantizer.py:471-497 pack_codes: code i in bits
+// [i*b, (i+1)*b) of the plane, least-significant bit first, each plane padded
+// to a whole byte) -> uint16 planes on the device (the loader never
+// materialises uint16 planes on the host)
+__global__ void unpack_packed_kernel(const uint8_t* __restrict__ packed, int64_t plane_bytes,
+                                     int m, int64_t per_plane, int b,
+                                     uint16_t* __restrict__ out) {
+    const int64_t total = (int64_t)m * per_plane;
+    const uint32_t mask = (1u << b) - 1u;
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
+         o += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = o / per_plane, i = o - t * per_plane;
+        const uint8_t* pl = packed + t * plane_bytes;
+        const int64_t bit = i * b;
+        const int64_t byte = bit >> 3;
+        const int sh = (int)(bit & 7);
+        uint32_t w = pl[byte];
+        if (sh + b > 8) w |= (uint32_t)pl[byte + 1] << 8;
+        if (sh + b > 16) w |= (uint32_t)pl[byte + 2] << 16;
+        out[o] = (uint16_t)((w >> sh) & mask);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Psumbook build into shared memory (shared by the fused kernel and the dump)
 //
@@ -1528,6 +1551,13 @@ cudaError_t launch_strict_gemm(const Plan& p, const uint8_t* packed, const uint1
     strict_gemm_kernel<<<(unsigned)blocks, threads, 0, s>>>(
         packed, raw16, books, scales, x, y, p.rows, p.segs, p.v, p.m, p.kcount, p.groups,
         p.g_eff, n, p.u, p.n_rg);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_packed(const uint8_t* packed, int64_t plane_bytes, int m,
+                                 int64_t per_plane, int b, uint16_t* out, cudaStream_t s) {
+    unpack_packed_kernel<<<grid_for((int64_t)m * per_plane, 256), 256, 0, s>>>(
+        packed, plane_bytes, m, per_plane, b, out);
     return cudaGetLastError();
 }
 

@@ -154,6 +154,21 @@ class DeviceLayer:
         _lib.check(lib.cg_layer_query(handle, ctypes.byref(info)))
         self.info = info.as_dict()
 
+    @classmethod
+    def _from_handle(cls, handle, rows: int, cols: int, cfg):
+        """Wrap a handle made by another creator (storage.load_device_layer)."""
+        self = cls.__new__(cls)
+        self.rows, self.cols = int(rows), int(cols)
+        self.row_range = (0, self.rows)
+        self.v, self.m, self.b, self.g = int(cfg.v), int(cfg.m), int(cfg.b), int(cfg.g)
+        self._keep = None
+        self._handle = handle
+        self._lib = _lib.load()
+        info = _lib.LayerInfo()
+        _lib.check(self._lib.cg_layer_query(handle, ctypes.byref(info)))
+        self.info = info.as_dict()
+        return self
+
     # -- lifetime -----------------------------------------------------------
     def close(self) -> None:
         h = getattr(self, "_handle", None)
