@@ -735,7 +735,17 @@ __device__ __forceinline__ void signal_rows(const GroupParams& p, CtaState& cs) 
 // have arrived on its row groups and sums them.  The wait is only on tasks of
 // earlier layers (or at kernel end), which never wait on us: no deadlock.
 // Last-arriver mode (grids beyond one wave): whoever arrives last sums.
-__device__ void close_task(const GroupParams& p, unsigned char* smem_raw, int tid) {
+__device__ __noinline__ void close_task_slow(const GroupParams& p, unsigned char* smem_raw, int tid);
+
+// (the common case -- nothing to close -- stays inline; the deterministic
+// split-K sums are out of line, keeping the hot kernel body small)
+__device__ __forceinline__ void close_task(const GroupParams& p, unsigned char* smem_raw, int tid) {
+    const CtaState& cs = *reinterpret_cast<const CtaState*>(smem_raw + p.off_bar);
+    if (cs.prev_layer < 0) return;
+    close_task_slow(p, smem_raw, tid);
+}
+
+__device__ __noinline__ void close_task_slow(const GroupParams& p, unsigned char* smem_raw, int tid) {
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
     const PrevTask prev{cs.prev_layer, cs.prev_slice, cs.prev_rg0, cs.prev_rg1};
     if (prev.layer < 0) return;
@@ -1103,6 +1113,26 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
     __syncthreads();
 }
 
+// this CTA's task list (thread 0, once per launch)
+__device__ __noinline__ void enumerate_tasks(const GroupParams& p, CtaState& cs, TaskCoord c,
+                                             bool have) {
+    int cnt = 0;
+    if (!have) {
+        cs.n_tl = 0;
+        return;
+    }
+    TaskCoord e = c;
+    bool more = true;
+    while (more && cnt < kTaskList) {
+        cs.tl_l[cnt] = e.l;
+        cs.tl_t[cnt] = e.t;
+        cs.tl_g[cnt] = (int)e.g;
+        ++cnt;
+        more = next_task_s(cs, p.n_layers, p.n_stages, e);
+    }
+    cs.n_tl = more ? kTaskList + 1 : cnt;  // kTaskList + 1: list full, more follow
+}
+
 // A launch runs a chain of stages (all layers share the tiling u: one
 // instantiation per (v, m, u, code width)); the layers of one stage are independent
 // (a grouped launch: {q,k,v}, {gate,up}), stage s+1 may read what stage s
@@ -1141,21 +1171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // weights of the first task (and its code range into L2) travel
         // before the wait on the previous kernel
         if (have) issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, true, false);
-        int cnt = 0;
-        if (have) {
-            TaskCoord e = c;
-            bool more = true;
-            while (more && cnt < kTaskList) {
-                cs.tl_l[cnt] = e.l;
-                cs.tl_t[cnt] = e.t;
-                cs.tl_g[cnt] = (int)e.g;
-                ++cnt;
-                more = next_task_s(cs, p.n_layers, p.n_stages, e);
-            }
-            cs.n_tl = more ? kTaskList + 1 : cnt;  // kTaskList + 1: list full, more follow
-        } else {
-            cs.n_tl = 0;
-        }
+        enumerate_tasks(p, cs, c, have);
     }
     // every layer's x (and y, for write-after-read) belongs to earlier work
     pdl_wait();
@@ -1180,11 +1196,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // zero this CTA's share of every split layer's output; each warp
         // releases its own stores (arrival 1: one unit per warp), so no CTA
         // barrier sits on this path -- the first flush waits for the grid
-        // (static layer indices: parameter loads with immediate offsets)
         bool any = false;
-#pragma unroll
-        for (int l = 0; l < kMaxGroup; ++l) {
-            if (l >= p.n_layers) break;
+#pragma unroll 1
+        for (int l = 0; l < p.n_layers; ++l) {
             const LayerTask& L = p.layer[l];
             if (L.n_slices <= 1) continue;
             any = true;
