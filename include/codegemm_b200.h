@@ -73,6 +73,15 @@ extern "C" {
                                    last-bit differences between runs)                  */
 
 typedef struct cg_layer cg_layer;
+typedef struct cg_comm cg_comm;
+
+#define CG_IPC_HANDLE_BYTES 64 /* cudaIpcMemHandle_t */
+
+/* cg_gemm_stages_xchg per-layer flags */
+#define CG_XCHG_PUSH 1 /* y is this rank's rows of a row-sharded layer, inside the comm
+                          buffer: after its stage they are copied to every peer      */
+#define CG_XCHG_WAIT 2 /* x (CG_X_F32, inside the comm buffer) was gathered by earlier
+                          launches: wait for every rank's rows before reading it      */
 
 typedef struct cg_layer_options {
     int u;             /* segments per lane per K-slice (1, 2, 4); 0 = planner choice */
@@ -135,7 +144,7 @@ int cg_layer_query(const cg_layer* layer, cg_layer_info* info);
 int cg_layer_gemm(cg_layer* layer, const void* x, int n, float* y, int mode, void* stream);
 
 /*
- * Grouped launch: y_i = W_i x_i for `count` (1..64) independent layers in ONE
+ * Grouped launch: y_i = W_i x_i for `count` (1..16) independent layers in ONE
  * launch of the fused kernel (e.g. the q/k/v or gate/up projections of a
  * decoder block, which read the same x).  Layers must share v, m, the code
  * width class (b <= 4 or b <= 8) and the device, and must all have
@@ -147,7 +156,7 @@ int cg_gemm_group(cg_layer* const* layers, const void* const* xs, float* const* 
 
 /*
  * Dependency-staged launch: one persistent launch of the fused kernel runs
- * `count` (1..64) layers in stages; stages[i] is layer i's stage (starts at 0,
+ * `count` (1..16) layers in stages; stages[i] is layer i's stage (starts at 0,
  * non-decreasing, steps of at most 1).  Layers of one stage are independent
  * (a grouped launch); a stage may read what earlier stages wrote -- e.g. a
  * decoder-block chain {q} -> {o} -> {gate,up} -> {down}.  x_dtypes[i] (NULL =
@@ -162,6 +171,40 @@ int cg_gemm_group(cg_layer* const* layers, const void* const* xs, float* const* 
  */
 int cg_gemm_stages(cg_layer* const* layers, const void* const* xs, const int* x_dtypes,
                    float* const* ys, const int* stages, int count, int n, void* stream);
+
+/*
+ * Row-shard exchange (the per-layer all-gather of the
+ * row-sharded layers, fused into the staged kernel over NVLink peer memory).
+ * Each rank (one process per GPU, or several ranks of one process for tests)
+ * creates a comm whose device buffer holds the GATHERED outputs (all rows of
+ * a sharded layer, same offsets on every rank).  A rank's layer writes its rows
+ * into that buffer (ys[i] = buffer + rank's row offset) with CG_XCHG_PUSH;
+ * once the layer's stage is complete on this rank, the kernel stores those rows
+ * into every peer's buffer (P2P stores) and releases a system-scope arrival
+ * counter on every rank.  A later stage whose x is the gathered buffer waits
+ * for every rank's arrivals before reading it (no NCCL call, no extra launch);
+ * a later launch reading it marks the layer CG_XCHG_WAIT.  Launch-completion
+ * counters keep a rank from overwriting a peer's buffer before that peer has
+ * finished its previous launch.  Every rank must issue the same sequence of
+ * comm launches (the counters count arrivals of `world` ranks x `ctas` CTAs).
+ *   world, rank : 1..8 ranks;  bytes: gathered-buffer bytes (same on every rank)
+ *   ctas        : CTAs per launch (0 = every SM); ranks of one GPU split it
+ *   timeout_ms  : a wait on peers longer than this traps the kernel (0 = none)
+ */
+int cg_comm_create(int world, int rank, int64_t bytes, int ctas, int timeout_ms, int device,
+                   cg_comm** out);
+int cg_comm_buffer(const cg_comm* comm, void** out);  /* the gathered-buffer base */
+/* 64-byte IPC handle of this rank's region; exchange them (e.g. all_gather_object) */
+int cg_comm_ipc_handle(const cg_comm* comm, void* out);
+/* map the peers' regions: handles = world x CG_IPC_HANDLE_BYTES in rank order */
+int cg_comm_open_peers(cg_comm* comm, const void* handles);
+/* ranks of one process: peers[r] = rank r's comm (peers[rank] == comm) */
+int cg_comm_set_peers(cg_comm* comm, cg_comm* const* peers);
+int cg_comm_destroy(cg_comm* comm);
+/* cg_gemm_stages plus xchg[i] = CG_XCHG_* flags of layer i; the launch runs comm's grid */
+int cg_gemm_stages_xchg(cg_layer* const* layers, const void* const* xs, const int* x_dtypes,
+                        float* const* ys, const int* stages, const int* xchg, int count, int n,
+                        cg_comm* comm, void* stream);
 
 /* Same with HOST buffers: copies x in, runs, copies y out, synchronises. */
 int cg_layer_gemm_host(cg_layer* layer, const uint16_t* x, int n, float* y, int mode,

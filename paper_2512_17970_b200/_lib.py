@@ -43,6 +43,13 @@ EXPORTS = (
     "cg_layer_destroy",
     "cg_layer_query",
     "cg_gemm_stages",
+    "cg_gemm_stages_xchg",
+    "cg_comm_create",
+    "cg_comm_buffer",
+    "cg_comm_ipc_handle",
+    "cg_comm_open_peers",
+    "cg_comm_set_peers",
+    "cg_comm_destroy",
     "cg_layer_gemm",
     "cg_layer_gemm_host",
     "cg_gemm_group",
@@ -122,6 +129,23 @@ def load() -> ctypes.CDLL:
                                    ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp),
                                    ctypes.POINTER(ctypes.c_int), i, i, vp]
     lib.cg_gemm_stages.restype = i
+    lib.cg_gemm_stages_xchg.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp),
+                                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                        i, i, vp, vp]
+    lib.cg_gemm_stages_xchg.restype = i
+    lib.cg_comm_create.argtypes = [i, i, ctypes.c_int64, i, i, i, ctypes.POINTER(vp)]
+    lib.cg_comm_create.restype = i
+    lib.cg_comm_buffer.argtypes = [vp, ctypes.POINTER(vp)]
+    lib.cg_comm_buffer.restype = i
+    lib.cg_comm_ipc_handle.argtypes = [vp, p]
+    lib.cg_comm_ipc_handle.restype = i
+    lib.cg_comm_open_peers.argtypes = [vp, p]
+    lib.cg_comm_open_peers.restype = i
+    lib.cg_comm_set_peers.argtypes = [vp, ctypes.POINTER(vp)]
+    lib.cg_comm_set_peers.restype = i
+    lib.cg_comm_destroy.argtypes = [vp]
+    lib.cg_comm_destroy.restype = i
     lib.cg_layer_gemm_host.argtypes = [vp, p, i, p, i, vp]
     lib.cg_layer_gemm_host.restype = i
     lib.cg_layer_psumbook.argtypes = [vp, p, i, p, vp]

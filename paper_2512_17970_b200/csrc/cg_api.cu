@@ -197,6 +197,19 @@ struct cg_layer {
     int64_t device_bytes = 0;
 };
 
+// One rank's row-shard exchange region (cg_comm_*): a header of counters and
+// barrier flags (cg::kXc*), then `bytes` of gathered buffers; the peers' regions
+// mapped into this process (CUDA IPC) or, for ranks of one process, given directly.
+struct cg_comm {
+    int world = 1, rank = 0, ctas = 0, device = 0;
+    unsigned char* base = nullptr;  // cudaMalloc: header + data
+    int64_t bytes = 0;              // data bytes after the header
+    unsigned char* peer[cg::kMaxRanks] = {nullptr};
+    bool ipc[cg::kMaxRanks] = {false};  // peer[r] opened with cudaIpcOpenMemHandle
+    bool linked = false;
+    unsigned long long timeout_ns = 0;
+};
+
 namespace {
 
 template <typename T>
@@ -293,7 +306,8 @@ cg::LayerTask task_of(const cg_layer* L, const uint16_t* x, float* y) {
 // stages[i] = dependency stage of layer i (non-decreasing; NULL = all stage 0).
 int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const* ys,
                   const int* stages, int count, int n, cudaStream_t s,
-                  const int* x_dtypes = nullptr) {
+                  const int* x_dtypes = nullptr, const int* xchg = nullptr,
+                  cg_comm* comm = nullptr) {
     if (count < 1 || count > cg::kMaxGroup)
         return fail(CG_ERR_ARG, "group size %d outside 1..%d", count, cg::kMaxGroup);
     const cg::Plan& p0 = layers[0]->plan;
@@ -341,6 +355,44 @@ int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* con
         if ((reinterpret_cast<uintptr_t>(xs[i]) & 15) || (p.cols % 8)) x_copy = false;
     }
     gp.n_stages = prev_stage + 1;
+    // ---- row-shard exchange: pushed y / gathered x must lie in the comm region
+    if (comm) {
+        if (!comm->linked) return fail(CG_ERR_ARG, "comm peers not opened / set");
+        if (comm->device != layers[0]->device)
+            return fail(CG_ERR_ARG, "comm and layers are on different devices");
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(comm->base) + cg::kXcHeader;
+        const uintptr_t hi = lo + (uintptr_t)comm->bytes;
+        for (int i = 0; i < count; ++i) {
+            const int f = xchg ? xchg[i] : 0;
+            if (f & ~(cg::kXchgPush | cg::kXchgWait))
+                return fail(CG_ERR_ARG, "xchg[%d] = %d: unknown bits", i, f);
+            cg::LayerTask& t = gp.layer[i];
+            t.xchg = f;
+            if (f & cg::kXchgPush) {
+                const uintptr_t a = reinterpret_cast<uintptr_t>(t.y);
+                if (a < lo || a + (uintptr_t)(t.rows * n * 4) > hi)
+                    return fail(CG_ERR_ARG, "layer %d: pushed y is not inside the comm buffer", i);
+            }
+            if (f & cg::kXchgWait) {
+                const uintptr_t a = reinterpret_cast<uintptr_t>(t.x32);
+                if (!t.x32 || a < lo || a + (uintptr_t)(t.cols * n * 4) > hi)
+                    return fail(CG_ERR_ARG,
+                                "layer %d: gathered x must be CG_X_F32 inside the comm buffer", i);
+            }
+        }
+        gp.xc_local = comm->base;
+        gp.xc_world = comm->world;
+        gp.xc_rank = comm->rank;
+        gp.xc_timeout_ns = comm->timeout_ns;
+        for (int r = 0; r < comm->world; ++r) {
+            gp.xc_peer[r] = comm->peer[r];
+            gp.xc_delta[r] = (long long)(reinterpret_cast<intptr_t>(comm->peer[r]) -
+                                         reinterpret_cast<intptr_t>(comm->base));
+        }
+    } else if (xchg) {
+        for (int i = 0; i < count; ++i)
+            if (xchg[i]) return fail(CG_ERR_ARG, "xchg[%d] set without a comm", i);
+    }
     // ---- dependencies (optional): a layer whose x IS an earlier stage's y (same
     //      pointer, float32, matching shape) waits for the row groups it reads
     //      instead of a grid barrier.  Only when every later-stage layer's x is either
@@ -352,7 +404,7 @@ int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* con
         // more than one barrier; kept for the row-local chains of later rounds)
         const char* rd = std::getenv("CG_ROW_DEPS");
         bool ok = gp.n_stages > 1 && !(layers[0]->flags & CG_OPT_DETERMINISTIC) && rd &&
-                  std::atoi(rd) != 0;
+                  std::atoi(rd) != 0 && !comm;
         for (int i = 0; i < count; ++i) gp.layer[i].dep = -1;
         for (int i = 0; ok && i < count; ++i) {
             cg::LayerTask& t = gp.layer[i];
@@ -384,8 +436,10 @@ int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* con
     //      it): minimise waves x (per-task cost + rows per task), the per-task
     //      cost (table build, input round trip, flush) expressed in row groups
     //      of gather work.  Layers created with an explicit rg_per_task keep it.
+    // (a comm launch runs the comm's grid on every rank: its barrier flags and
+    // exchange counters count arrivals of exactly that many CTAs)
+    const int sms = comm ? comm->ctas : layers[0]->sms;
     {
-        const int sms = layers[0]->sms;
         bool forced = false;
         // columns the per-task smem buffers scale with: reduce-add mode adds the
         // partials of several columns straight into y (no staging)
@@ -438,8 +492,8 @@ int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* con
     // barrier flags rely on every launch making the same arrivals on every
     // CTA); if a layer has more tasks than CTAs, a CTA runs several tasks of it
     // and deterministic split-K falls back to last-arriver sums
-    if (grid > layers[0]->sms) gp.flags |= cg::kFlagLastArriver;
-    grid = layers[0]->sms;
+    if (grid > sms) gp.flags |= cg::kFlagLastArriver;
+    grid = sms;
     // fix-up list / owned-ticket targets (deterministic) or the staging buffer
     // of a task's partial rows (reduce-add): the larger of the two
     const int cap = rg_max * n + 16;
@@ -464,8 +518,12 @@ int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* con
     gp.off_stage[0] = lay.off_list;
     gp.off_stage[1] = lay.off_stage1;
     gp.list_cap = cap;
-    gp.grid_flags = layers[0]->grid_flags;
+    gp.grid_flags = comm ? reinterpret_cast<unsigned long long*>(comm->base + cg::kXcFlags)
+                         : layers[0]->grid_flags;
     if (!x_copy) gp.flags |= cg::kFlagXRegs;
+    // ranks sharing one GPU (comm->ctas < SMs) must run concurrently: no
+    // cooperative attribute (it may serialise their grids); each grid fits
+    if (comm && comm->ctas < layers[0]->sms) gp.flags |= cg::kFlagDbgNoCoop;
     if (layers[0]->flags & CG_OPT_DETERMINISTIC) gp.flags |= cg::kFlagDeterministic;
     if (const char* e = std::getenv("CG_DEBUG_FLAGS")) gp.flags |= std::atoi(e);
     const bool pdl = !(layers[0]->flags & CG_OPT_NO_PDL) && !(gp.flags & cg::kFlagDbgNoPdl);
@@ -781,6 +839,118 @@ int cg_gemm_stages(cg_layer* const* layers, const void* const* xs, const int* x_
     DeviceGuard guard(layers[0]->device);
     return launch_stages(layers, reinterpret_cast<const uint16_t* const*>(xs), ys, stages, count,
                          n, static_cast<cudaStream_t>(stream), x_dtypes);
+}
+
+int cg_gemm_stages_xchg(cg_layer* const* layers, const void* const* xs, const int* x_dtypes,
+                        float* const* ys, const int* stages, const int* xchg, int count, int n,
+                        cg_comm* comm, void* stream) {
+    if (!layers || !xs || !ys || !stages || !xchg || !comm)
+        return fail(CG_ERR_ARG, "NULL layers/xs/ys/stages/xchg/comm");
+    if (count < 1 || count > cg::kMaxGroup)
+        return fail(CG_ERR_ARG, "launch size %d outside 1..%d", count, cg::kMaxGroup);
+    if (n < 1) return fail(CG_ERR_SHAPE, "x must have >= 1 column, got %d", n);
+    for (int i = 0; i < count; ++i)
+        if (!layers[i] || !xs[i] || !ys[i]) return fail(CG_ERR_ARG, "NULL entry %d", i);
+    DeviceGuard guard(layers[0]->device);
+    return launch_stages(layers, reinterpret_cast<const uint16_t* const*>(xs), ys, stages, count,
+                         n, static_cast<cudaStream_t>(stream), x_dtypes, xchg, comm);
+}
+
+int cg_comm_create(int world, int rank, int64_t bytes, int ctas, int timeout_ms, int device,
+                   cg_comm** out) {
+    if (!out) return fail(CG_ERR_ARG, "NULL out");
+    *out = nullptr;
+    if (world < 1 || world > cg::kMaxRanks)
+        return fail(CG_ERR_ARG, "world %d outside 1..%d", world, cg::kMaxRanks);
+    if (rank < 0 || rank >= world) return fail(CG_ERR_ARG, "rank %d outside 0..%d", rank, world - 1);
+    if (bytes < 0 || timeout_ms < 0) return fail(CG_ERR_ARG, "negative bytes / timeout");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(CG_ERR_CUDA, "no CUDA device available; this library has no CPU path");
+    if (device < 0) cudaGetDevice(&device);
+    if (device >= ndev) return fail(CG_ERR_ARG, "device %d of %d", device, ndev);
+    DeviceGuard guard(device);
+    const int sms = sm_count_of(device);
+    if (ctas == 0) ctas = sms;
+    if (ctas < 1 || ctas > sms || ctas > cg::kMaxCtas)
+        return fail(CG_ERR_ARG, "ctas %d outside 1..%d", ctas, std::min(sms, cg::kMaxCtas));
+    cg_comm* c = new cg_comm;
+    c->world = world;
+    c->rank = rank;
+    c->ctas = ctas;
+    c->device = device;
+    c->bytes = (bytes + 255) & ~int64_t(255);
+    c->timeout_ns = (unsigned long long)timeout_ms * 1000000ull;
+    cudaError_t e = cudaMalloc(&c->base, (size_t)(cg::kXcHeader + c->bytes));
+    if (e == cudaSuccess) e = cudaMemset(c->base, 0, (size_t)(cg::kXcHeader + c->bytes));
+    if (e != cudaSuccess) {
+        cudaFree(c->base);
+        delete c;
+        return cuda_fail(e, "comm region alloc");
+    }
+    c->peer[rank] = c->base;
+    if (world == 1) c->linked = true;
+    *out = c;
+    return CG_OK;
+}
+
+int cg_comm_buffer(const cg_comm* c, void** out) {
+    if (!c || !out) return fail(CG_ERR_ARG, "NULL comm/out");
+    *out = c->base + cg::kXcHeader;
+    return CG_OK;
+}
+
+int cg_comm_ipc_handle(const cg_comm* c, void* out) {
+    if (!c || !out) return fail(CG_ERR_ARG, "NULL comm/out");
+    static_assert(sizeof(cudaIpcMemHandle_t) == CG_IPC_HANDLE_BYTES, "IPC handle size");
+    DeviceGuard guard(c->device);
+    cudaIpcMemHandle_t h;
+    CG_CUDA(cudaIpcGetMemHandle(&h, c->base), "IPC handle");
+    std::memcpy(out, &h, sizeof(h));
+    return CG_OK;
+}
+
+int cg_comm_open_peers(cg_comm* c, const void* handles) {
+    if (!c || !handles) return fail(CG_ERR_ARG, "NULL comm/handles");
+    if (c->linked) return fail(CG_ERR_ARG, "comm peers already set");
+    DeviceGuard guard(c->device);
+    const unsigned char* h = static_cast<const unsigned char*>(handles);
+    for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) continue;
+        cudaIpcMemHandle_t ih;
+        std::memcpy(&ih, h + (size_t)r * CG_IPC_HANDLE_BYTES, sizeof(ih));
+        void* ptr = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr, ih, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return cuda_fail(e, "IPC open of a peer region");
+        c->peer[r] = static_cast<unsigned char*>(ptr);
+        c->ipc[r] = true;
+    }
+    c->linked = true;
+    return CG_OK;
+}
+
+int cg_comm_set_peers(cg_comm* c, cg_comm* const* peers) {
+    if (!c || !peers) return fail(CG_ERR_ARG, "NULL comm/peers");
+    if (c->linked && c->world > 1) return fail(CG_ERR_ARG, "comm peers already set");
+    for (int r = 0; r < c->world; ++r) {
+        const cg_comm* q = peers[r];
+        if (!q || q->world != c->world || q->rank != r || q->bytes != c->bytes || q->ctas != c->ctas)
+            return fail(CG_ERR_ARG, "peers[%d] is not rank %d of a matching comm", r, r);
+        if (r == c->rank && q != c) return fail(CG_ERR_ARG, "peers[%d] must be this comm", r);
+    }
+    for (int r = 0; r < c->world; ++r) c->peer[r] = peers[r]->base;
+    c->linked = true;
+    return CG_OK;
+}
+
+int cg_comm_destroy(cg_comm* c) {
+    if (!c) return CG_OK;
+    DeviceGuard guard(c->device);
+    for (int r = 0; r < c->world; ++r)
+        if (c->ipc[r]) cudaIpcCloseMemHandle(c->peer[r]);
+    cudaFree(c->base);
+    delete c;
+    return CG_OK;
 }
 
 int cg_layer_gemm_host(cg_layer* L, const uint16_t* x, int n, float* y, int mode, void* stream) {

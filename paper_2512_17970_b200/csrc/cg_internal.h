@@ -42,7 +42,23 @@ struct LayerTask {
     int dep;                  // layer whose y this layer's x is (row-group readiness), or -1
     unsigned long long* rg_cnt;  // [0] launches completed, [1 + rg] row-group completions
                                  // (this layer is a producer for a later layer), or null
+    int xchg;                 // kXchgPush | kXchgWait (row-shard exchange launches), else 0
 };
+
+// ---- row-shard exchange (cg_comm): every rank owns one device region; a
+//      layer's y (this rank's rows of a row-sharded layer) lives inside it at
+//      the same offset on every rank, so peer p's copy is y + xc_delta[p].
+constexpr int kXchgPush = 1;  // after the layer's stage, copy its rows to every peer
+constexpr int kXchgWait = 2;  // x is a gathered buffer of an earlier launch: wait first
+constexpr int kMaxRanks = 8;
+constexpr int kMaxCtas = 256;
+// the region's header (bytes from its base), then the gathered buffers
+constexpr int kXcArrive = 0;       // u64: push arrivals (one per CTA per exchange per rank)
+constexpr int kXcDone = 128;       // u64: launch completions (one per CTA per launch per rank)
+constexpr int kXcFlags = 256;      // u64[16 + kMaxCtas]: this rank's grid-barrier flags
+constexpr int kXcOwnX = 4096;      // u64[kMaxCtas]: exchanges CTA c took part in
+constexpr int kXcOwnL = 6144;      // u64[kMaxCtas]: launches CTA c took part in
+constexpr int kXcHeader = 8192;
 
 constexpr int kMaxGroup = 16;
 
@@ -64,6 +80,12 @@ struct GroupParams {
     int off_stage[2];         // split-K staging of a task's partial rows (reduce-add), x2
     unsigned long long* grid_flags;   // per-CTA barrier flags (zero barrier, stage barriers)
     unsigned long long* stamps;  // diagnostics: per-CTA phase timestamps (8 per CTA) or null
+    // row-shard exchange (null xc_local: none)
+    unsigned char* xc_local;               // this rank's region base
+    unsigned char* xc_peer[kMaxRanks];     // every rank's region base (self included)
+    long long xc_delta[kMaxRanks];         // peer copy address - local address (bytes)
+    int xc_world, xc_rank;
+    unsigned long long xc_timeout_ns;      // trap a wait that exceeds it (0: wait forever)
 };
 
 // Psumbook dump (bit-exactness check of the fused kernel's on-chip table)

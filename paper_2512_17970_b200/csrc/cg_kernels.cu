@@ -631,7 +631,7 @@ struct FixupEntry {
 // mbarrier, the fix-up count, the previous task (closed at the start of the
 // next task, after that task's input loads are in flight, or at kernel end)
 // and the zero-barrier generation.
-constexpr int kTaskList = 40;
+constexpr int kTaskList = 36;
 struct CtaState {
     uint64_t in_bar[2];           // mbarriers of the two task-input buffers
     int list_count;
@@ -649,6 +649,9 @@ struct CtaState {
     // must not walk the layer table: indexed parameter loads are slow)
     int l_stage[kMaxGroup], l_tasks[kMaxGroup];  // per layer, copied from the parameters
     unsigned long long l_gen[kMaxGroup];  // producer layers: completed launches (row deps)
+    // row-shard exchange: counts at launch start, exchanges made, stages that push
+    unsigned long long xc_base, xc_launch;
+    int xc_n, xc_pushed, xc_push_mask;
     int n_tl;                     // entries (kTaskList = more tasks follow)
     int tl_l[kTaskList], tl_g[kTaskList];
     long long tl_t[kTaskList];
@@ -1084,12 +1087,101 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
 #undef CG_STAMP
 }
 
+// ---- row-shard exchange over peer memory (NVLink P2P stores) ----
+// Counters in each rank's region header, written by every rank's CTAs with
+// system-scope release reductions and polled with system-scope acquires:
+// kXcArrive gains one per CTA per rank per exchange (an exchange is complete
+// at (exchanges so far) * world * grid), kXcDone one per CTA per rank per
+// launch (a rank may write into a peer's buffers once every rank finished
+// reading its previous launch's).  Per-CTA counts at launch start come from
+// the CTA's own slots (kXcOwnX / kXcOwnL), written at kernel end.
+__device__ __forceinline__ void xc_wait(const GroupParams& p, int off, unsigned long long want) {
+    const unsigned long long* a = reinterpret_cast<const unsigned long long*>(p.xc_local + off);
+    unsigned long long f, t0 = 0;
+    while (true) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(a) : "memory");
+        if (f >= want) break;
+        if (p.xc_timeout_ns) {
+            const unsigned long long t = gtimer();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > p.xc_timeout_ns) __trap();  // a peer never arrived
+        }
+        __nanosleep(64);
+    }
+}
+__device__ __forceinline__ void xc_signal(const GroupParams& p, int off) {
+    for (int r = 0; r < p.xc_world; ++r)
+        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(p.xc_peer[r] + off) : "memory");
+}
+// thread 0, after griddepcontrol.wait: this CTA's counts, the pushing stages,
+// and -- if a layer reads a buffer gathered by earlier launches -- the wait
+// for every rank's pushes so far
+__device__ __noinline__ void xc_prologue(const GroupParams& p, CtaState& cs) {
+    const unsigned long long* own_x =
+        reinterpret_cast<const unsigned long long*>(p.xc_local + kXcOwnX);
+    const unsigned long long* own_l =
+        reinterpret_cast<const unsigned long long*>(p.xc_local + kXcOwnL);
+    cs.xc_base = own_x[blockIdx.x];
+    cs.xc_launch = own_l[blockIdx.x];
+    cs.xc_n = 0;
+    cs.xc_pushed = 0;
+    int mask = 0;
+    bool wait = false;
+    for (int l = 0; l < p.n_layers; ++l) {
+        if (p.layer[l].xchg & kXchgPush) mask |= 1 << p.layer[l].stage;
+        wait |= (p.layer[l].xchg & kXchgWait) != 0;
+    }
+    cs.xc_push_mask = mask;
+    if (wait) xc_wait(p, kXcArrive, cs.xc_base * p.xc_world * gridDim.x);
+}
+// all threads, after the grid barrier that closed `stage`: copy this CTA's
+// share of the stage's pushed layers to every peer, release, signal
+__device__ __noinline__ void xc_push(const GroupParams& p, unsigned char* smem_raw, int stage,
+                                     int tid) {
+    CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
+    if (!cs.xc_pushed) {  // every rank is done reading its previous launch
+        if (tid == 0)
+            xc_wait(p, kXcDone, cs.xc_launch * (unsigned long long)p.xc_world * gridDim.x);
+        __syncthreads();
+    }
+    for (int l = 0; l < p.n_layers; ++l) {
+        const LayerTask& L = p.layer[l];
+        if (L.stage != stage || !(L.xchg & kXchgPush)) continue;
+        const int64_t elems = L.rows * p.n;
+        const int64_t per = (((elems + gridDim.x - 1) / gridDim.x) + 3) & ~int64_t(3);
+        const int64_t e0 = min((int64_t)blockIdx.x * per, elems), e1 = min(e0 + per, elems);
+        const bool vec = (reinterpret_cast<uintptr_t>(L.y) & 15) == 0;
+        const int64_t body = vec ? e0 + ((e1 - e0) & ~int64_t(3)) : e0;
+        for (int64_t e = e0 + 4 * tid; e < body; e += 4 * kThreads) {
+            const float4 v = __ldcg(reinterpret_cast<const float4*>(L.y + e));
+            for (int r = 0; r < p.xc_world; ++r)
+                if (r != p.xc_rank)
+                    *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(L.y + e) +
+                                               p.xc_delta[r]) = v;
+        }
+        for (int64_t e = body + tid; e < e1; e += kThreads) {
+            const float v = __ldcg(L.y + e);
+            for (int r = 0; r < p.xc_world; ++r)
+                if (r != p.xc_rank)
+                    *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(L.y + e) +
+                                              p.xc_delta[r]) = v;
+        }
+    }
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+        xc_signal(p, kXcArrive);
+        cs.xc_pushed = 1;
+        ++cs.xc_n;
+    }
+}
+
 // Grid barrier between dependent stages of a launch (sense reversal on
 // {count, generation}).  Everything this CTA wrote in the stage -- plain
 // stores and the bulk (async-proxy) reduce-adds -- is complete and released
 // before the arrival; the next stage's x, read by TMA, is acquired after.
 __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned char* smem_raw,
-                                              int tid) {
+                                              int tid, int stage, bool final = false) {
     __syncthreads();
     close_task(p, smem_raw, tid);  // deterministic split-K: pending ordered sums
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
@@ -1111,6 +1203,16 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
         ++cs.n_bar;
     }
     __syncthreads();
+    if (p.xc_local && ((cs.xc_push_mask >> stage) & 1)) {
+        // row-shard exchange: the stage's rows to every peer, then (unless the
+        // launch ends here) every rank's rows before the next stage reads them
+        xc_push(p, smem_raw, stage, tid);
+        if (!final && tid == 0) {
+            xc_wait(p, kXcArrive, (cs.xc_base + cs.xc_n) * (unsigned long long)p.xc_world * gridDim.x);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncthreads();
+    }
 }
 
 // this CTA's task list (thread 0, once per launch)
@@ -1185,6 +1287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      : "memory");
         cs.l_gen[tid] = gv;
     }
+    if (tid == 0 && p.xc_local) xc_prologue(p, cs);
     if (tid == 32) {  // barrier state (used by thread 0 after the prologue barrier)
         unsigned long long b;
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(b)
@@ -1227,7 +1330,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 zero_arrive(p, tid);
                 zero_todo = false;
             }
-            if (!(p.flags & kFlagRowDeps)) stage_barrier(p, smem_raw, tid);
+            if (!(p.flags & kFlagRowDeps)) stage_barrier(p, smem_raw, tid, stage);
             ++stage;
             if (tid == 0 && have && stage == target)
                 issue_inputs<V, M, U, KB>(p, c, buf, smem_raw, false, true);
@@ -1255,6 +1358,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         have = has_next;
     }
     if (zero_todo) zero_arrive(p, tid);  // (a CTA without any task)
+    // the last stage's rows to the peers (its consumers wait in a later launch)
+    if (p.xc_local && ((cs.xc_push_mask >> (p.n_stages - 1)) & 1))
+        stage_barrier(p, smem_raw, tid, p.n_stages - 1, true);
     // close the last task's row groups; drain the bulk reduce-adds
     __syncthreads();
     close_task(p, smem_raw, tid);
@@ -1274,6 +1380,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.grid_flags + 16 + blockIdx.x),
                      "l"(cs.bar_base + (unsigned long long)kBarUnits * cs.n_arrive)
                      : "memory");
+        if (p.xc_local) {  // exchange counts for the next launch; this rank is done reading
+            reinterpret_cast<unsigned long long*>(p.xc_local + kXcOwnX)[blockIdx.x] =
+                cs.xc_base + (unsigned long long)cs.xc_n;
+            reinterpret_cast<unsigned long long*>(p.xc_local + kXcOwnL)[blockIdx.x] = cs.xc_launch + 1;
+            xc_signal(p, kXcDone);
+        }
     }
     __syncthreads();
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 127] = gtimer();

@@ -268,7 +268,7 @@ def gemm_group(layers, xs, ys=None, stream=None):
     return ys
 
 
-def gemm_stages(layers, xs, ys, stages, stream=None):
+def gemm_stages(layers, xs, ys, stages, stream=None, *, xchg=None, comm=None):
     """One persistent launch running dependent stages of layers (cg_gemm_stages).
 
     ``stages[i]`` is layer i's stage (0, then non-decreasing by steps of <= 1);
@@ -278,6 +278,12 @@ def gemm_stages(layers, xs, ys, stages, stream=None):
     in the same launch -- rounded to binary16 (RNE) as it is read.  ``ys`` are
     preallocated (rows_i, n) float32 CUDA tensors.  All layers share v, m,
     code width and tiling u.
+
+    With ``comm`` (a ``dist.PeerExchange``) the launch also runs the row-shard
+    exchange (cg_gemm_stages_xchg): ``xchg[i]`` is ``dist.XCHG_PUSH`` (y_i is
+    this rank's rows inside the comm buffer, copied to every peer after its
+    stage) and/or ``dist.XCHG_WAIT`` (x_i is a buffer gathered by an earlier
+    launch).
     """
     import torch
 
@@ -299,7 +305,17 @@ def gemm_stages(layers, xs, ys, stages, stream=None):
     xd = (ctypes.c_int * k)(*[1 if x.dtype == torch.float32 else 0 for x in xs])
     yp = (ctypes.c_void_p * k)(*[y.data_ptr() for y in ys])
     st = (ctypes.c_int * k)(*[int(v) for v in stages])
-    _lib.check(lib.cg_gemm_stages(hs, xp, xd, yp, st, k, n, ctypes.c_void_p(s.cuda_stream)))
+    if comm is None:
+        if xchg is not None and any(xchg):
+            raise ConfigError("xchg flags need a comm")
+        _lib.check(lib.cg_gemm_stages(hs, xp, xd, yp, st, k, n, ctypes.c_void_p(s.cuda_stream)))
+        return ys
+    flags = list(xchg) if xchg is not None else [0] * k
+    if len(flags) != k:
+        raise ShapeError("need one xchg flag per layer")
+    xf = (ctypes.c_int * k)(*[int(f) for f in flags])
+    _lib.check(lib.cg_gemm_stages_xchg(hs, xp, xd, yp, st, xf, k, n, comm.handle,
+                                       ctypes.c_void_p(s.cuda_stream)))
     return ys
 
 
