@@ -284,7 +284,8 @@ def main():
         return
 
     import paper_2512_17970_b200 as cg
-    from paper_2512_17970_b200.dist import ShardedLayer
+    from paper_2512_17970_b200.dist import (XCHG_PUSH, GatheredLayout, PeerExchange,
+                                            ShardedLayer)
     from oracle import codegemm_oracle as orc
 
     torch.cuda.set_device(local_rank)
@@ -299,7 +300,8 @@ def main():
         layers = []
         for idx, (name, rows, cols) in enumerate(spec):
             q = make_layer(rows, cols, cfg, layer_seed(cp, idx, rows, cols))
-            sl = ShardedLayer(q, rank, world) if world > 1 else cg.DeviceLayer(q, u=TILING_U)
+            sl = (ShardedLayer(q, rank, world, u=TILING_U) if world > 1
+                  else cg.DeviceLayer(q, u=TILING_U))
             x = torch.from_numpy(orc.bench_input_array(cols, n, cp * 31 + idx)).to(dev)
             per = sl.per if world > 1 else rows
             layers.append({"name": name, "rows": rows, "cols": cols, "layer": sl, "x": x,
@@ -309,6 +311,27 @@ def main():
 
     def dev_layer(L):
         return L["layer"].device_layer if world > 1 else L["layer"]
+
+    # N > 1: the all-gather fused into the staged launch (cg_gemm_stages_xchg):
+    # every layer's gathered output lives in one peer-mapped region per rank;
+    # each stage's rows are stored into every peer's copy over NVLink and the
+    # next stage reads the gathered x once every rank arrived
+    if world > 1:
+        glay = GatheredLayout([r for _ in blocks for (_, r, c) in spec], n, world)
+        comm = PeerExchange(world, rank, glay.nbytes, timeout_ms=60000, device=local_rank)
+        comm.connect()
+        nl = len(spec)
+        for cp, b in enumerate(blocks):
+            for i, L in enumerate(b):
+                L["g_local"] = glay.local(comm, cp * nl + i)
+                L["g_full"] = glay.gathered(comm, cp * nl + i)
+                assert L["g_local"].shape[0] == L["layer"].r1 - L["layer"].r0
+
+    def run_xchg(b):
+        """The whole row-sharded block in ONE launch per rank, all-gathers fused in."""
+        xs = [b[i]["x"] if src is None else b[src]["g_full"] for i, src in enumerate(STEP_XSRC)]
+        cg.gemm_stages([dev_layer(L) for L in b], xs, [L["g_local"] for L in b],
+                       list(STEP_STAGES), xchg=[XCHG_PUSH] * len(b), comm=comm)
 
     def run_kernel(L):
         dl = dev_layer(L)
@@ -379,9 +402,9 @@ def main():
         singles = [capture(lambda b=b: run_staged(b)) for b in blocks]
         launches_per_step = 1.0 / CHAIN
     else:
-        graphs = [capture(lambda b=b: [run_group(b, g) for g in groups]) for b in blocks]
+        graphs = [capture(lambda b=b: run_xchg(b)) for b in blocks]
         singles = None
-        launches_per_step = len(groups)
+        launches_per_step = 1
 
     def timed(replays, count, per_graph=1):
         """Replay graphs[i % len] until `count` steps (per_graph steps per replay) ran;
@@ -430,12 +453,13 @@ def main():
     timed(sep, 3 * spg, spg)
     ms_sep = timed(sep, reps, spg) / reps
     del sep
-    ms_grp = None
     if world == 1:
         grp = [capture(lambda: [run_group(b, g) for b in blocks for g in groups])]
-        timed(grp, 3 * spg, spg)
-        ms_grp = timed(grp, reps, spg) / reps
-        del grp
+    else:  # grouped launches + an NCCL all-gather per layer (the unfused path)
+        grp = [capture(lambda b=b: [run_group(b, g) for g in groups]) for b in blocks]
+    timed(grp, 3 * spg, spg)
+    ms_grp = timed(grp, reps, spg) / reps
+    del grp
 
     # ---- per-shape kernel microseconds: graphs of R back-to-back launches of
     #      one shape (rotating weight copies), so host launch cost is amortised
@@ -512,14 +536,22 @@ def main():
                                             "us_per_launch": round(dom_us, 3),
                                             "GB/s": round(dom_bytes / (dom_us * 1e-6) / 1e9, 1)}}
     else:
+        # one kernel per step per rank: the staged exchange launch over this
+        # rank's rows (algorithmic bytes of its shards; x and gathered y included)
+        rank_bytes = sum(layer_bytes(L["layer"].r1 - L["layer"].r0, L["cols"], cfg, n)
+                         for L in blocks[0])
+        achieved = rank_bytes / (ms_per_step * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "frac": round(achieved / peak, 4), "traffic": None,
                     "peak_source": peak_src,
-                    "kernel": f"group_gemv_kernel {dom} {dom_rows // world}x{dom_cols} "
-                              f"(u={dl_dom.info['u']}, tasks={dl_dom.info['n_tasks']}), "
-                              f"{R} back-to-back launches per graph",
-                    "us_per_launch": round(dom_us, 3), "bytes_per_launch": dom_bytes,
-                    "frac_of_8TBs_nominal": round(achieved / 8000.0, 4)}
+                    "kernel": f"group_gemv_kernel<v{cfg['v']},m{cfg['m']},u{TILING_U}> staged "
+                              f"exchange launch per rank ({len(spec)} row-sharded layers, "
+                              f"{len(groups)} stages, all-gathers fused); per-GPU",
+                    "us_per_launch": round(ms_per_step * 1e3, 3), "bytes_per_launch": rank_bytes,
+                    "frac_of_8TBs_nominal": round(achieved / 8000.0, 4),
+                    "largest_layer_alone": {"layer": f"{dom} {dom_rows // world}x{dom_cols}",
+                                            "us_per_launch": round(dom_us, 3),
+                                            "GB/s": round(dom_bytes / (dom_us * 1e-6) / 1e9, 1)}}
 
     # ---- end to end through the reference-facing C ABI with host buffers
     e2e_steps = max(3, min(args.steps, 100))
@@ -527,28 +559,24 @@ def main():
     h2d = sum(x.nbytes for x in host_x)
     d2h = sum(4 * r * n for (_, r, c) in spec)
 
-    if world == 1:
-        # one step = H2D of the step's inputs (x of q,k,v) from pinned memory,
-        # the staged launch, D2H of every layer's output, synchronise
-        host_x = [torch.from_numpy(orc.bench_input_array(c, n, 100 + i)).pin_memory()
-                  if STEP_XSRC[i] is None else None for i, (_, r, c) in enumerate(spec)]
-        host_y = [torch.empty((r, n), dtype=torch.float32).pin_memory() for (_, r, c) in spec]
-        h2d = sum(x.numel() * 2 for x in host_x if x is not None)
+    # one step = H2D of the step's inputs (x of q,k,v) from pinned memory, the
+    # staged launch, D2H of every layer's (gathered) output, synchronise
+    host_x = [torch.from_numpy(orc.bench_input_array(c, n, 100 + i)).pin_memory()
+              if STEP_XSRC[i] is None else None for i, (_, r, c) in enumerate(spec)]
+    host_y = [torch.empty((r, n), dtype=torch.float32).pin_memory() for (_, r, c) in spec]
+    h2d = sum(x.numel() * 2 for x in host_x if x is not None)
 
     def e2e_step(b):
+        for i, xh in enumerate(host_x):
+            if xh is not None:
+                b[i]["x"].copy_(xh, non_blocking=True)
         if world == 1:
-            for i, xh in enumerate(host_x):
-                if xh is not None:
-                    b[i]["x"].copy_(xh, non_blocking=True)
             run_staged(b)
-            for L, yh in zip(b, host_y):
-                yh.copy_(L["y"], non_blocking=True)
-            torch.cuda.synchronize(dev)
-            return
-        for L, xh in zip(b, host_x):
-            xt = torch.from_numpy(xh).to(dev, non_blocking=False)
-            y = L["layer"].forward(xt)
-            y.cpu()
+        else:
+            run_xchg(b)
+        for L, yh in zip(b, host_y):
+            yh.copy_(L["y"] if world == 1 else L["g_full"], non_blocking=True)
+        torch.cuda.synchronize(dev)
 
     e2e_step(blocks[0])
     if world > 1:
@@ -567,7 +595,9 @@ def main():
            "ms_per_step": round(e2e_s / e2e_steps * 1e3, 3),
            "path": "gemm_stages per step (pinned H2D of the step inputs, one staged launch, "
                    "pinned D2H of all 7 layer outputs, sync)"
-           if world == 1 else "ShardedLayer.forward per layer (H2D x, kernels, NCCL all-gather, D2H y)"}
+           if world == 1 else "gemm_stages(xchg, comm) per step (pinned H2D of the step inputs, "
+                              "one staged exchange launch, pinned D2H of all 7 gathered outputs, "
+                              "sync)"}
 
     base = base_c = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -587,7 +617,8 @@ def main():
                        "layers_per_step": len(spec), "weight_copies": copies,
                        "l2": f"inputs larger than L2: {copies} distinct block copies rotated "
                              f"({copies * weight_bytes / 2**20:.0f} MiB of weights per rank)",
-                       "parallelism": f"rows sharded over {world} GPUs + NCCL all-gather"
+                       "parallelism": f"rows sharded over {world} GPUs, all-gathers fused "
+                                      "into the kernel over NVLink peer stores"
                        if world > 1 else "single GPU",
                        "launch": ("one persistent staged launch (cg_gemm_stages) per "
                                   f"{CHAIN} steps: {CHAIN} block copies chained "
@@ -596,8 +627,10 @@ def main():
                                   "y and the next block's q,k,v read y_down, rounded to fp16; "
                                   f"grid barriers between stages, u={TILING_U}; CUDA graph")
                        if world == 1 else
-                       "per step: 4 grouped fused launches ({q,k,v} {o} {gate,up} {down}) + "
-                       "NCCL all-gather per layer, CUDA graph per block copy, PDL"},
+                       "per step: ONE staged exchange launch per rank (cg_gemm_stages_xchg): "
+                       "stages {q,k,v} -> {o} -> {gate,up} -> {down}, every layer's rows "
+                       "pushed to every peer after its stage, the next stage reading the "
+                       "gathered y; CUDA graph per block copy, PDL"},
             "us_per_layer": us_per_layer,
             "us_per_layer_staged_chain": us_chain,
             "us_per_block": round(ms_per_step * 1e3, 3),
@@ -607,9 +640,10 @@ def main():
             "separate_launches": {"us_per_block": round(ms_sep * 1e3, 3),
                                   "value": round(step_bytes / (ms_sep / 1e3) / 1e9, 2),
                                   "launches_per_step": len(spec)},
-            "grouped_launches": None if ms_grp is None else
-            {"us_per_block": round(ms_grp * 1e3, 3),
-             "value": round(step_bytes / (ms_grp / 1e3) / 1e9, 2), "launches_per_step": len(groups)},
+            "grouped_launches": {"us_per_block": round(ms_grp * 1e3, 3),
+                                 "value": round(step_bytes / (ms_grp / 1e3) / 1e9, 2),
+                                 "launches_per_step": len(groups),
+                                 "all_gather": None if world == 1 else "NCCL, one per layer"},
             "roofline": roofline,
             "cpu_baseline": base, "cpu_baseline_c": base_c,
             "e2e": e2e,

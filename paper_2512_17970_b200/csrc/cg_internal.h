@@ -53,11 +53,9 @@ constexpr int kXchgWait = 2;  // x is a gathered buffer of an earlier launch: wa
 constexpr int kMaxRanks = 8;
 constexpr int kMaxCtas = 256;
 // the region's header (bytes from its base), then the gathered buffers
-constexpr int kXcArrive = 0;       // u64: push arrivals (one per CTA per exchange per rank)
-constexpr int kXcDone = 128;       // u64: launch completions (one per CTA per launch per rank)
+constexpr int kXcArrive = 0;       // u64: exchange arrivals (one per CTA per exchange per rank)
 constexpr int kXcFlags = 256;      // u64[16 + kMaxCtas]: this rank's grid-barrier flags
 constexpr int kXcOwnX = 4096;      // u64[kMaxCtas]: exchanges CTA c took part in
-constexpr int kXcOwnL = 6144;      // u64[kMaxCtas]: launches CTA c took part in
 constexpr int kXcHeader = 8192;
 
 constexpr int kMaxGroup = 16;
@@ -105,6 +103,7 @@ constexpr int kFlagXRegs = 32;  // x staged through registers (unaligned x / odd
 // diagnostics only (CG_DEBUG_FLAGS): wrong results, phase isolation for timing
 constexpr int kFlagRowDeps = 64;  // stages ordered by row-group readiness, not grid barriers
 constexpr int kFlagDirectAdd = 1 << 14;  // split-K partials red.add'ed into y even at n == 1
+constexpr int kFlagDbgXcGpuScope = 1 << 15; // exchange fences at gpu scope (ranks of one GPU only)
 constexpr int kFlagDbgSkipBuild = 1 << 8;   // no Psumbook build
 constexpr int kFlagDbgNoLoads = 1 << 9;     // gather reuses the preloaded code tiles
 constexpr int kFlagDbgSkipGather = 1 << 10; // no gather

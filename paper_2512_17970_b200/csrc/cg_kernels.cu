@@ -631,7 +631,7 @@ struct FixupEntry {
 // mbarrier, the fix-up count, the previous task (closed at the start of the
 // next task, after that task's input loads are in flight, or at kernel end)
 // and the zero-barrier generation.
-constexpr int kTaskList = 36;
+constexpr int kTaskList = 32;
 struct CtaState {
     uint64_t in_bar[2];           // mbarriers of the two task-input buffers
     int list_count;
@@ -648,10 +648,14 @@ struct CtaState {
     // this CTA's task list, enumerated once at kernel start (task switches
     // must not walk the layer table: indexed parameter loads are slow)
     int l_stage[kMaxGroup], l_tasks[kMaxGroup];  // per layer, copied from the parameters
-    unsigned long long l_gen[kMaxGroup];  // producer layers: completed launches (row deps)
+    union {
+        unsigned long long l_gen[kMaxGroup];  // producer layers: completed launches (row deps)
+        float* xc_y[kMaxGroup];               // exchange launches (no row deps): y per layer
+    };
+    int xc_elems[kMaxGroup];      // exchange: elements of y per layer (rows * n)
     // row-shard exchange: counts at launch start, exchanges made, stages that push
-    unsigned long long xc_base, xc_launch;
-    int xc_n, xc_pushed, xc_push_mask;
+    unsigned long long xc_base;
+    int xc_n, xc_pushed, xc_push_mask, xc_layer_mask;
     int n_tl;                     // entries (kTaskList = more tasks follow)
     int tl_l[kTaskList], tl_g[kTaskList];
     long long tl_t[kTaskList];
@@ -1088,30 +1092,43 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
 }
 
 // ---- row-shard exchange over peer memory (NVLink P2P stores) ----
-// Counters in each rank's region header, written by every rank's CTAs with
-// system-scope release reductions and polled with system-scope acquires:
-// kXcArrive gains one per CTA per rank per exchange (an exchange is complete
-// at (exchanges so far) * world * grid), kXcDone one per CTA per rank per
-// launch (a rank may write into a peer's buffers once every rank finished
-// reading its previous launch's).  Per-CTA counts at launch start come from
-// the CTA's own slots (kXcOwnX / kXcOwnL), written at kernel end.
-__device__ __forceinline__ void xc_wait(const GroupParams& p, int off, unsigned long long want) {
-    const unsigned long long* a = reinterpret_cast<const unsigned long long*>(p.xc_local + off);
+// One counter in each rank's region header (kXcArrive), written by every
+// rank's CTAs with a system-scope fence + reductions and polled with
+// system-scope acquires: it gains one per CTA per rank per exchange, so
+// exchange k (counted over all launches on the comm) is complete at
+// k * world * grid.  Every launch ends with an exchange (its last stage's rows,
+// or none), made after all of the rank's reads: a rank writes into a peer's
+// buffers only after every rank's previous exchanges -- hence previous
+// launches -- are complete.  Per-CTA exchange counts at launch start come from
+// the CTA's own slot (kXcOwnX), written at kernel end.
+__device__ __forceinline__ void xc_fence(bool gpu_scope) {
+    if (gpu_scope) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    else asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+// (arguments by value: called from out-of-line code, where every parameter
+// access would be a generic load)
+__device__ __forceinline__ void xc_wait(const unsigned long long* a, unsigned long long want,
+                                        bool gpu_scope, unsigned long long timeout_ns) {
     unsigned long long f, t0 = 0;
     while (true) {
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(a) : "memory");
+        if (gpu_scope) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(a) : "memory");
+        else asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(a) : "memory");
         if (f >= want) break;
-        if (p.xc_timeout_ns) {
+        if (timeout_ns) {
             const unsigned long long t = gtimer();
             if (t0 == 0) t0 = t;
-            else if (t - t0 > p.xc_timeout_ns) __trap();  // a peer never arrived
+            else if (t - t0 > timeout_ns) __trap();  // a peer never arrived
         }
         __nanosleep(64);
     }
 }
+// one thread, after a CTA barrier that ordered the CTA's accesses before it:
+// one fence releases them all, then plain reductions on every rank's counter
 __device__ __forceinline__ void xc_signal(const GroupParams& p, int off) {
+    const bool gs = (p.flags & kFlagDbgXcGpuScope) != 0;
+    xc_fence(gs);
     for (int r = 0; r < p.xc_world; ++r)
-        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(p.xc_peer[r] + off) : "memory");
+        asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(p.xc_peer[r] + off) : "memory");
 }
 // thread 0, after griddepcontrol.wait: this CTA's counts, the pushing stages,
 // and -- if a layer reads a buffer gathered by earlier launches -- the wait
@@ -1119,61 +1136,62 @@ __device__ __forceinline__ void xc_signal(const GroupParams& p, int off) {
 __device__ __noinline__ void xc_prologue(const GroupParams& p, CtaState& cs) {
     const unsigned long long* own_x =
         reinterpret_cast<const unsigned long long*>(p.xc_local + kXcOwnX);
-    const unsigned long long* own_l =
-        reinterpret_cast<const unsigned long long*>(p.xc_local + kXcOwnL);
     cs.xc_base = own_x[blockIdx.x];
-    cs.xc_launch = own_l[blockIdx.x];
     cs.xc_n = 0;
     cs.xc_pushed = 0;
-    int mask = 0;
+    int mask = 0, lmask = 0;
     bool wait = false;
     for (int l = 0; l < p.n_layers; ++l) {
-        if (p.layer[l].xchg & kXchgPush) mask |= 1 << p.layer[l].stage;
-        wait |= (p.layer[l].xchg & kXchgWait) != 0;
+        const LayerTask& L = p.layer[l];
+        if (L.xchg & kXchgPush) {
+            mask |= 1 << L.stage;
+            lmask |= 1 << l;
+        }
+        cs.xc_y[l] = L.y;
+        cs.xc_elems[l] = (int)(L.rows * p.n);
+        wait |= (L.xchg & kXchgWait) != 0;
     }
     cs.xc_push_mask = mask;
-    if (wait) xc_wait(p, kXcArrive, cs.xc_base * p.xc_world * gridDim.x);
+    cs.xc_layer_mask = lmask;
+    if (wait)
+        xc_wait(reinterpret_cast<const unsigned long long*>(p.xc_local + kXcArrive),
+                cs.xc_base * p.xc_world * gridDim.x, (p.flags & kFlagDbgXcGpuScope) != 0,
+                p.xc_timeout_ns);
 }
 // all threads, after the grid barrier that closed `stage`: copy this CTA's
-// share of the stage's pushed layers to every peer, release, signal
-__device__ __noinline__ void xc_push(const GroupParams& p, unsigned char* smem_raw, int stage,
-                                     int tid) {
-    CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
-    if (!cs.xc_pushed) {  // every rank is done reading its previous launch
-        if (tid == 0)
-            xc_wait(p, kXcDone, cs.xc_launch * (unsigned long long)p.xc_world * gridDim.x);
+// share of the stage's pushed layers to every peer, release, signal (at the
+// end of the launch also with nothing to push)
+__device__ __noinline__ void xc_push(unsigned char* smem_raw, int off_bar, int stage, int tid,
+                                     int n_layers, int world, int rank, const long long* deltas,
+                                     const unsigned long long* arrive, bool gpu_scope,
+                                     unsigned long long timeout_ns) {
+    CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + off_bar);
+    if (!((cs.xc_push_mask >> stage) & 1)) return;  // (a launch's closing arrival: nothing to push)
+    if (!cs.xc_pushed) {
+        // the first stores into peers' buffers in this launch: every rank has
+        // finished its previous launches (and their reads)
+        if (tid == 0) xc_wait(arrive, cs.xc_base * (unsigned long long)world * gridDim.x, gpu_scope,
+                              timeout_ns);
         __syncthreads();
     }
-    for (int l = 0; l < p.n_layers; ++l) {
-        const LayerTask& L = p.layer[l];
-        if (L.stage != stage || !(L.xchg & kXchgPush)) continue;
-        const int64_t elems = L.rows * p.n;
-        const int64_t per = (((elems + gridDim.x - 1) / gridDim.x) + 3) & ~int64_t(3);
-        const int64_t e0 = min((int64_t)blockIdx.x * per, elems), e1 = min(e0 + per, elems);
-        const bool vec = (reinterpret_cast<uintptr_t>(L.y) & 15) == 0;
-        const int64_t body = vec ? e0 + ((e1 - e0) & ~int64_t(3)) : e0;
-        for (int64_t e = e0 + 4 * tid; e < body; e += 4 * kThreads) {
-            const float4 v = __ldcg(reinterpret_cast<const float4*>(L.y + e));
-            for (int r = 0; r < p.xc_world; ++r)
-                if (r != p.xc_rank)
-                    *reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(L.y + e) +
-                                               p.xc_delta[r]) = v;
-        }
-        for (int64_t e = body + tid; e < e1; e += kThreads) {
-            const float v = __ldcg(L.y + e);
-            for (int r = 0; r < p.xc_world; ++r)
-                if (r != p.xc_rank)
-                    *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(L.y + e) +
-                                              p.xc_delta[r]) = v;
+    for (int r = 0; r < world; ++r) {
+        if (r == rank) continue;
+        const long long d = deltas[r];
+        for (int l = 0; l < n_layers; ++l) {
+            if (cs.l_stage[l] != stage || !((cs.xc_layer_mask >> l) & 1)) continue;
+            float* y = cs.xc_y[l];
+            const int elems = cs.xc_elems[l];
+            const int per = (((elems + (int)gridDim.x - 1) / (int)gridDim.x) + 3) & ~3;
+            const int e0 = min((int)blockIdx.x * per, elems), e1 = min(e0 + per, elems);
+            const bool vec = (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+            const int body = vec ? e0 + ((e1 - e0) & ~3) : e0;
+            float* dst = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(y) + d);
+            for (int e = e0 + 4 * tid; e < body; e += 4 * kThreads)
+                *reinterpret_cast<float4*>(dst + e) = __ldcg(reinterpret_cast<const float4*>(y + e));
+            for (int e = body + tid; e < e1; e += kThreads) dst[e] = __ldcg(y + e);
         }
     }
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
     __syncthreads();
-    if (tid == 0) {
-        xc_signal(p, kXcArrive);
-        cs.xc_pushed = 1;
-        ++cs.xc_n;
-    }
 }
 
 // Grid barrier between dependent stages of a launch (sense reversal on
@@ -1203,13 +1221,29 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
         ++cs.n_bar;
     }
     __syncthreads();
-    if (p.xc_local && ((cs.xc_push_mask >> stage) & 1)) {
+    if (p.xc_local && (((cs.xc_push_mask >> stage) & 1) || final)) {
         // row-shard exchange: the stage's rows to every peer, then (unless the
         // launch ends here) every rank's rows before the next stage reads them
-        xc_push(p, smem_raw, stage, tid);
+        const bool gs = (p.flags & kFlagDbgXcGpuScope) != 0;
+        const unsigned long long* arrive =
+            reinterpret_cast<const unsigned long long*>(p.xc_local + kXcArrive);
+        xc_push(smem_raw, p.off_bar, stage, tid, p.n_layers, p.xc_world, p.xc_rank, p.xc_delta,
+                arrive, gs, p.xc_timeout_ns);
+        if (tid == 0) {
+            // (the system-scope fence in here is the exchange's main cost: ~1.1 us
+            // idle, ~4.5 us inside the kernel -- tools/micro/membar.cu, stamps)
+            xc_signal(p, kXcArrive);
+            cs.xc_pushed |= (cs.xc_push_mask >> stage) & 1;
+            ++cs.xc_n;
+        }
+        unsigned long long* xst = (p.stamps && stage < 4) ? p.stamps + blockIdx.x * 128 + 112 + 2 * stage
+                                                          : nullptr;
+        if (xst && tid == 0) xst[0] = gtimer();
         if (!final && tid == 0) {
-            xc_wait(p, kXcArrive, (cs.xc_base + cs.xc_n) * (unsigned long long)p.xc_world * gridDim.x);
+            xc_wait(arrive, (cs.xc_base + cs.xc_n) * (unsigned long long)p.xc_world * gridDim.x, gs,
+                    p.xc_timeout_ns);
             asm volatile("fence.proxy.async.global;" ::: "memory");
+            if (xst) xst[1] = gtimer();
         }
         __syncthreads();
     }
@@ -1358,9 +1392,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         have = has_next;
     }
     if (zero_todo) zero_arrive(p, tid);  // (a CTA without any task)
-    // the last stage's rows to the peers (its consumers wait in a later launch)
-    if (p.xc_local && ((cs.xc_push_mask >> (p.n_stages - 1)) & 1))
-        stage_barrier(p, smem_raw, tid, p.n_stages - 1, true);
+    // the last stage's rows to the peers (its consumers wait in a later
+    // launch); the arrival also tells the peers this rank is done reading
+    if (p.xc_local) stage_barrier(p, smem_raw, tid, p.n_stages - 1, true);
     // close the last task's row groups; drain the bulk reduce-adds
     __syncthreads();
     close_task(p, smem_raw, tid);
@@ -1380,12 +1414,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.grid_flags + 16 + blockIdx.x),
                      "l"(cs.bar_base + (unsigned long long)kBarUnits * cs.n_arrive)
                      : "memory");
-        if (p.xc_local) {  // exchange counts for the next launch; this rank is done reading
+        if (p.xc_local)  // exchange count for the next launch
             reinterpret_cast<unsigned long long*>(p.xc_local + kXcOwnX)[blockIdx.x] =
                 cs.xc_base + (unsigned long long)cs.xc_n;
-            reinterpret_cast<unsigned long long*>(p.xc_local + kXcOwnL)[blockIdx.x] = cs.xc_launch + 1;
-            xc_signal(p, kXcDone);
-        }
     }
     __syncthreads();
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 127] = gtimer();

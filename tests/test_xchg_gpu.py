@@ -169,3 +169,65 @@ def test_exchange_rejects_bad_arguments():
         cg.gemm_stages([dl], [x0], [y], [0], xchg=[PUSH | WAIT], comm=comm)
     with pytest.raises(cg.ConfigError):
         cg.gemm_stages([dl], [x0], [y], [0], xchg=[PUSH])
+
+
+_TWO_PROCESSES = r"""
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+import paper_2512_17970_b200 as cg
+from paper_2512_17970_b200 import dist as cgd
+import test_xchg_gpu as t
+
+rank, world = int(sys.argv[1]), 2
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=sys.argv[2])
+dist.init_process_group("gloo", rank=rank, world_size=world)
+torch.cuda.set_device(0)
+qs, x0 = t._qs(), t._x0()
+ref = t._single_gpu_chain(qs, x0, t.DET)
+sms = torch.cuda.get_device_properties(0).multi_processor_count
+lay = cgd.GatheredLayout([r for r, _ in t.SHAPES], 1, world)
+comm = cgd.PeerExchange(world, rank, lay.nbytes, ctas=sms // world, timeout_ms=20000)
+comm.connect()  # 64-byte CUDA IPC handles over the (gloo) process group
+layers = [cg.DeviceLayer(q, u=2, flags=t.DET, row_range=lay.bounds(i, rank))
+          for i, q in enumerate(qs)]
+for rep in range(3):
+    for i in range(3):
+        x = x0 if i == 0 else lay.gathered(comm, i - 1)
+        cg.gemm_stages([layers[i]], [x], [lay.local(comm, i)], [0],
+                       xchg=[t.PUSH | (t.WAIT if i else 0)], comm=comm)
+    torch.cuda.synchronize()
+    dist.barrier()
+    for i in range(3):
+        got = lay.gathered(comm, i).cpu().numpy()
+        assert np.array_equal(t.u32(got), t.u32(ref[i])), (rep, rank, i)
+    dist.barrier()
+comm.close()
+dist.destroy_process_group()
+print("OK", rank)
+"""
+
+
+def test_exchange_two_processes_cuda_ipc():
+    """Two processes (one GPU, time-sliced): the regions are mapped with
+    cudaIpcOpenMemHandle after a handle exchange over torch.distributed --
+    the one-process-per-GPU plumbing -- and each layer is one launch per rank."""
+    import socket
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = str(s.getsockname()[1])
+    procs = [subprocess.Popen([sys.executable, "-c", _TWO_PROCESSES, str(r), port], cwd=root,
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+             for r in range(2)]
+    outs = []
+    for p in procs:
+        try:
+            outs.append(p.communicate(timeout=600))
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            raise
+    for r, (p, (out, err)) in enumerate(zip(procs, outs)):
+        assert p.returncode == 0 and f"OK {r}" in out, out[-2000:] + err[-4000:]

@@ -20,6 +20,7 @@ from paper_2512_17970_b200 import _lib  # noqa: E402
 from oracle import codegemm_oracle as orc  # noqa: E402
 
 chain = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+XCHG = int(os.environ.get("XCHG", "0"))  # 1: through a world-1 comm, every layer pushed
 cfg = bench.CONFIGS["m1v4g128"]
 spec = bench.block_spec("8b")
 nl = len(spec)
@@ -27,8 +28,15 @@ sets = []
 for k in range(2):
     layers = [cg.DeviceLayer(bench.make_layer(r, c, cfg, 100 * k + 7 * j + i), u=bench.TILING_U or 4)
               for j in range(chain) for i, (_, r, c) in enumerate(spec)]
-    ys = [torch.empty((r, 1), dtype=torch.float32, device="cuda") for j in range(chain)
-          for (_, r, c) in spec]
+    if XCHG:
+        from paper_2512_17970_b200 import dist as cgd
+        glay = cgd.GatheredLayout([r for j in range(chain) for (_, r, c) in spec], 1, 1)
+        comm = cgd.PeerExchange(1, 0, glay.nbytes, timeout_ms=20000)
+        ys = [glay.gathered(comm, i) for i in range(chain * nl)]
+    else:
+        comm = None
+        ys = [torch.empty((r, 1), dtype=torch.float32, device="cuda") for j in range(chain)
+              for (_, r, c) in spec]
     x0 = torch.from_numpy(orc.bench_input_array(spec[0][2], 1, k)).cuda()
     xs, st = [], []
     for j in range(chain):
@@ -38,16 +46,16 @@ for k in range(2):
             else:
                 xs.append(x0 if j == 0 else ys[(j - 1) * nl + nl - 1])
             st.append(4 * j + bench.STEP_STAGES[i])
-    sets.append((layers, xs, ys, st))
+    sets.append((layers, xs, ys, st, comm))
 s = torch.cuda.Stream()
 with torch.cuda.stream(s):
-    for L, xs, ys, st in sets:
-        cg.gemm_stages(L, xs, ys, st, stream=s)
+    for L, xs, ys, st, cm in sets:
+        cg.gemm_stages(L, xs, ys, st, stream=s, comm=cm, xchg=[1] * len(L) if cm else None)
 s.synchronize()
 g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g, stream=s):
-    for L, xs, ys, st in sets:
-        cg.gemm_stages(L, xs, ys, st, stream=s)
+    for L, xs, ys, st, cm in sets:
+        cg.gemm_stages(L, xs, ys, st, stream=s, comm=cm, xchg=[1] * len(L) if cm else None)
 with torch.cuda.stream(s):
     for _ in range(3):
         g.replay()
@@ -86,4 +94,7 @@ for b in range(7):
     for j, nm in enumerate(("entered", "drained", "arrived", "released")):
         if j in (0, 3):
             show(f"barrier{b} {nm}", st[:, 96 + 4 * b + j])
+for b in range(4):
+    show(f"xchg{b} pushed", st[:, 112 + 2 * b])
+    show(f"xchg{b} all arrived", st[:, 113 + 2 * b])
 show("kernel end", st[:, 127])
