@@ -494,6 +494,12 @@ int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* con
     // and deterministic split-K falls back to last-arriver sums
     if (grid > sms) gp.flags |= cg::kFlagLastArriver;
     grid = sms;
+    for (int i = 0; i < count; ++i) {
+        const int64_t elems = gp.layer[i].rows * n;
+        if (elems >= (int64_t(1) << 31))
+            return fail(CG_ERR_SHAPE, "layer %d: rows * n = %lld exceeds 2^31", i, (long long)elems);
+        gp.layer[i].zero_per = (int)((((elems + grid - 1) / grid) + 3) & ~int64_t(3));
+    }
     // fix-up list / owned-ticket targets (deterministic) or the staging buffer
     // of a task's partial rows (reduce-add): the larger of the two
     const int cap = rg_max * n + 16;

@@ -43,6 +43,7 @@ struct LayerTask {
     unsigned long long* rg_cnt;  // [0] launches completed, [1 + rg] row-group completions
                                  // (this layer is a producer for a later layer), or null
     int xchg;                 // kXchgPush | kXchgWait (row-shard exchange launches), else 0
+    int zero_per;             // elements of y each CTA zeroes (rows * n / grid, rounded up to 4)
 };
 
 // ---- row-shard exchange (cg_comm): every rank owns one device region; a

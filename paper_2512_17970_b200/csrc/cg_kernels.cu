@@ -1249,24 +1249,42 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
     }
 }
 
-// this CTA's task list (thread 0, once per launch)
-__device__ __noinline__ void enumerate_tasks(const GroupParams& p, CtaState& cs, TaskCoord c,
-                                             bool have) {
-    int cnt = 0;
-    if (!have) {
-        cs.n_tl = 0;
-        return;
+// this CTA's task list (warp 1, once per launch, beside thread 0's input
+// issue): lane s counts the CTA's tasks in stage s (c, c + grid, ... below the
+// stage's task total), a prefix scan places the stages in the list, and each
+// lane locates list entries k = lane, lane + 32, ...  `scratch` is 48 ints of
+// shared memory that no task uses yet.
+__device__ __forceinline__ void enumerate_tasks(int n_layers, int n_stages, CtaState& cs,
+                                                int* scratch, int lane) {
+    const int G = gridDim.x, c = blockIdx.x;
+    int total_s = 0;
+    if (lane < n_stages)
+        for (int l = 0; l < n_layers; ++l)
+            if (cs.l_stage[l] == lane) total_s += cs.l_tasks[l];
+    const int cnt = (lane < n_stages && c < total_s) ? (total_s - c + G - 1) / G : 0;
+    int pre = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, pre, off);
+        if (lane >= off) pre += v;
     }
-    TaskCoord e = c;
-    bool more = true;
-    while (more && cnt < kTaskList) {
-        cs.tl_l[cnt] = e.l;
-        cs.tl_t[cnt] = e.t;
-        cs.tl_g[cnt] = (int)e.g;
-        ++cnt;
-        more = next_task_s(cs, p.n_layers, p.n_stages, e);
+    const int total = __shfl_sync(0xffffffffu, pre, 31);
+    if (lane < kMaxGroup) {
+        scratch[lane] = pre - cnt;  // first list slot of stage `lane`
+        scratch[16 + lane] = cnt;
     }
-    cs.n_tl = more ? kTaskList + 1 : cnt;  // kTaskList + 1: list full, more follow
+    __syncwarp();
+    const int n = min(total, kTaskList);
+    for (int k = lane; k < n; k += 32) {
+        int s = 0;
+        while (!(k >= scratch[s] && k < scratch[s] + scratch[16 + s])) ++s;
+        TaskCoord e;
+        locate_s(cs, n_layers, s, (int64_t)c + (int64_t)(k - scratch[s]) * G, e);
+        cs.tl_l[k] = e.l;
+        cs.tl_t[k] = e.t;
+        cs.tl_g[k] = (int)e.g;
+    }
+    if (lane == 0) cs.n_tl = total > kTaskList ? kTaskList + 1 : total;
 }
 
 // A launch runs a chain of stages (all layers share the tiling u: one
@@ -1290,9 +1308,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         cs.l_tasks[tid] = p.layer[tid].n_tasks;
     }
     __syncthreads();
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 116] = gtimer();
     TaskCoord c{0, 0, 0};
     bool have = false;
     for (int s = 0; s < p.n_stages && !have; ++s) have = locate_s(cs, p.n_layers, s, blockIdx.x, c);
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 117] = gtimer();
     if (tid == 0) {
         mbar_init(&cs.in_bar[0], 1);
         mbar_init(&cs.in_bar[1], 1);
@@ -1307,7 +1327,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // weights of the first task (and its code range into L2) travel
         // before the wait on the previous kernel
         if (have) issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, true, false);
-        enumerate_tasks(p, cs, c, have);
+        if (p.stamps) p.stamps[blockIdx.x * 128 + 118] = gtimer();
+    }
+    if (tid >= 32 && tid < 64) {
+        enumerate_tasks(p.n_layers, p.n_stages, cs, reinterpret_cast<int*>(smem_raw + p.off_list),
+                        tid & 31);
+        if (p.stamps && tid == 32) p.stamps[blockIdx.x * 128 + 123] = gtimer();
     }
     // every layer's x (and y, for write-after-read) belongs to earlier work
     pdl_wait();
@@ -1315,6 +1340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     if (tid == 0 && have && cs.l_stage[c.l] == 0)
         issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, false, true);
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 119] = gtimer();
     if (tid < p.n_layers && p.layer[tid].rg_cnt) {  // producer generations (row deps)
         unsigned long long gv;
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(gv) : "l"(p.layer[tid].rg_cnt)
@@ -1339,10 +1365,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const LayerTask& L = p.layer[l];
             if (L.n_slices <= 1) continue;
             any = true;
-            const int64_t elems = L.rows * p.n;
-            const int64_t per = (elems + gridDim.x - 1) / gridDim.x;
-            const int64_t e0 = blockIdx.x * per, e1 = min(e0 + per, elems);
-            for (int64_t e = e0 + tid; e < e1; e += kThreads) L.y[e] = 0.0f;
+            const int elems = (int)(L.rows * p.n), per = L.zero_per;
+            const int e0 = min((int)blockIdx.x * per, elems), e1 = min(e0 + per, elems);
+            float* y = L.y;
+            // (warps 0 and 1 issue the task inputs and list the tasks meanwhile)
+            for (int e = e0 + tid - 64; e < e1 && tid >= 64; e += kThreads - 64) y[e] = 0.0f;
         }
         // the arrival (fenced) is made after the CTA's first Psumbook build,
         // when these stores have long completed -- off the prologue's path

@@ -81,7 +81,12 @@ def show(name, col):
 
 
 show("kernel entry", st[:, 124])
+show("table copied", st[:, 116])
+show("first task located", st[:, 117])
+show("weights issued", st[:, 118])
+show("before pdl_wait (t0)", st[:, 123])
 show("pdl_wait passed", st[:, 126])
+show("x issued", st[:, 119])
 show("zeroing done (tid 0)", st[:, 122])
 show("prologue done", st[:, 125])
 names = [(0, "start"), (7, "synced"), (4, "inputs ok"), (5, "x staged"), (6, "table ready"),
