@@ -82,3 +82,32 @@ def test_shard_bounds_cover_rows_exactly():
                 assert 0 <= r0 <= r1 <= rows and r1 - r0 <= per
                 got.extend(range(r0, r1))
             assert got == list(range(rows))
+
+
+def test_gathered_layout_shards_cover_rows_aligned():
+    """Exchange buffer layout (dist.GatheredLayout): every layer's gathered
+    output at a 256-byte aligned offset; rank shards are whole 16-row groups,
+    contiguous, disjoint and cover the rows; each rank's slice starts 16-byte
+    aligned (the kernel's vector stores and bulk reduce-adds)."""
+    from paper_2512_17970_b200.dist import GatheredLayout, shard_bounds
+
+    rows = [4096, 1024, 1000, 14336, 48]
+    for world in (1, 2, 3, 4, 8):
+        for n in (1, 3):
+            lay = GatheredLayout(rows, n, world)
+            assert lay.nbytes >= sum(r * n * 4 for r in rows)
+            for i, r in enumerate(rows):
+                assert lay.offset[i] % 256 == 0
+                if i:
+                    assert lay.offset[i] >= lay.offset[i - 1] + rows[i - 1] * n * 4
+                covered = 0
+                for rank in range(world):
+                    r0, r1 = lay.bounds(i, rank)
+                    assert r0 == min(r, covered) and r0 <= r1 <= r
+                    if r1 > r0:
+                        assert r0 % 16 == 0
+                        assert (lay.offset[i] + r0 * n * 4) % 16 == 0
+                    covered = r1
+                assert covered == r
+    assert shard_bounds(100, 3, 1) == (34, 68, 34)
+    assert shard_bounds(100, 3, 1, align=16) == (48, 96, 48)
