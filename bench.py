@@ -294,20 +294,36 @@ def main():
     weight_bytes = sum(layer_bytes(r, c, cfg, n, with_io=False) for (_, r, c) in spec) // world
     copies = max(2, -(-3 * L2_BYTES // max(1, weight_bytes)))
 
-    # ---- layers: `copies` distinct copies of the block, rows sharded over ranks
-    blocks = []
+    # ---- layers: `copies` distinct copies of the block, rows sharded over ranks.
+    #      A block's inputs (the x of q,k,v) and its outputs are views of one
+    #      contiguous buffer each, so the end-to-end step moves them with one copy
+    #      each way.
+    in_elems = sum(c * n for i, (_, r, c) in enumerate(spec) if STEP_XSRC[i] is None)
+    blocks, xbufs, ybufs = [], [], []
     for cp in range(copies):
         layers = []
+        xbuf = torch.empty(in_elems, dtype=torch.float16, device=dev)
+        ybuf = torch.empty(sum(-(-r // world) * world * n for (_, r, c) in spec),
+                           dtype=torch.float32, device=dev)
+        xo = yo = 0
         for idx, (name, rows, cols) in enumerate(spec):
             q = make_layer(rows, cols, cfg, layer_seed(cp, idx, rows, cols))
             sl = (ShardedLayer(q, rank, world, u=TILING_U) if world > 1
                   else cg.DeviceLayer(q, u=TILING_U))
             x = torch.from_numpy(orc.bench_input_array(cols, n, cp * 31 + idx)).to(dev)
+            if STEP_XSRC[idx] is None:
+                xbuf[xo: xo + cols * n].copy_(x.view(-1))
+                x = xbuf[xo: xo + cols * n].view(cols, n)
+                xo += cols * n
             per = sl.per if world > 1 else rows
+            y = ybuf[yo: yo + per * world * n].view(per * world, n)
+            yo += per * world * n
             layers.append({"name": name, "rows": rows, "cols": cols, "layer": sl, "x": x,
                            "y_local": torch.empty((per, n), dtype=torch.float32, device=dev),
-                           "y": torch.empty((per * world, n), dtype=torch.float32, device=dev)})
+                           "y": y})
         blocks.append(layers)
+        xbufs.append(xbuf)
+        ybufs.append(ybuf)
 
     def dev_layer(L):
         return L["layer"].device_layer if world > 1 else L["layer"]
@@ -327,11 +343,17 @@ def main():
                 L["g_full"] = glay.gathered(comm, cp * nl + i)
                 assert L["g_local"].shape[0] == L["layer"].r1 - L["layer"].r0
 
+    prepared = {}  # one prepared launch (marshalled once) per block copy
+
     def run_xchg(b):
         """The whole row-sharded block in ONE launch per rank, all-gathers fused in."""
-        xs = [b[i]["x"] if src is None else b[src]["g_full"] for i, src in enumerate(STEP_XSRC)]
-        cg.gemm_stages([dev_layer(L) for L in b], xs, [L["g_local"] for L in b],
-                       list(STEP_STAGES), xchg=[XCHG_PUSH] * len(b), comm=comm)
+        key = ("x", id(b))
+        if key not in prepared:
+            xs = [b[i]["x"] if src is None else b[src]["g_full"] for i, src in enumerate(STEP_XSRC)]
+            prepared[key] = cg.StagedLaunch([dev_layer(L) for L in b], xs,
+                                            [L["g_local"] for L in b], list(STEP_STAGES),
+                                            xchg=[XCHG_PUSH] * len(b), comm=comm)
+        prepared[key]()
 
     def run_kernel(L):
         dl = dev_layer(L)
@@ -370,8 +392,12 @@ def main():
 
     def run_staged(b):
         """The whole block in one launch: stage chain with real data dependencies."""
-        xs = [b[i]["x"] if src is None else b[src]["y"] for i, src in enumerate(STEP_XSRC)]
-        cg.gemm_stages([L["layer"] for L in b], xs, [L["y"] for L in b], list(STEP_STAGES))
+        key = ("s", id(b))
+        if key not in prepared:
+            xs = [b[i]["x"] if src is None else b[src]["y"] for i, src in enumerate(STEP_XSRC)]
+            prepared[key] = cg.StagedLaunch([L["layer"] for L in b], xs, [L["y"] for L in b],
+                                            list(STEP_STAGES))
+        prepared[key]()
 
     CHAIN = int(os.environ.get("CG_BENCH_CHAIN", "1"))  # blocks per launch (<= 16 layers)
 
@@ -553,37 +579,41 @@ def main():
                                             "us_per_launch": round(dom_us, 3),
                                             "GB/s": round(dom_bytes / (dom_us * 1e-6) / 1e9, 1)}}
 
-    # ---- end to end through the reference-facing C ABI with host buffers
+    # ---- end to end through the public API with host buffers
     e2e_steps = max(3, min(args.steps, 100))
-    host_x = [orc.bench_input_array(c, n, 100 + i) for i, (_, r, c) in enumerate(spec)]
-    h2d = sum(x.nbytes for x in host_x)
-    d2h = sum(4 * r * n for (_, r, c) in spec)
+    # one step = H2D of the step's inputs (x of q,k,v: one contiguous buffer) from
+    # pinned memory, the staged launch (prepared), D2H of every layer's (gathered)
+    # output (one contiguous range), synchronise
+    host_x = torch.from_numpy(np.concatenate(
+        [orc.bench_input_array(c, n, 100 + i).reshape(-1) for i, (_, r, c) in enumerate(spec)
+         if STEP_XSRC[i] is None])).pin_memory()
+    if world == 1:
+        out_views = [ybufs[cp] for cp in range(len(blocks))]
+    else:  # this block's gathered outputs: one range of the comm region
+        nl = len(spec)
+        out_views = []
+        for cp in range(len(blocks)):
+            a, z = glay.offset[cp * nl], glay.offset[cp * nl + nl - 1] + spec[-1][1] * n * 4
+            out_views.append(comm.view(a, (z - a) // 4, 1).view(-1))
+    host_y = torch.empty(out_views[0].numel(), dtype=torch.float32).pin_memory()
+    h2d = host_x.numel() * 2
+    d2h = host_y.numel() * 4
 
-    # one step = H2D of the step's inputs (x of q,k,v) from pinned memory, the
-    # staged launch, D2H of every layer's (gathered) output, synchronise
-    host_x = [torch.from_numpy(orc.bench_input_array(c, n, 100 + i)).pin_memory()
-              if STEP_XSRC[i] is None else None for i, (_, r, c) in enumerate(spec)]
-    host_y = [torch.empty((r, n), dtype=torch.float32).pin_memory() for (_, r, c) in spec]
-    h2d = sum(x.numel() * 2 for x in host_x if x is not None)
+    for cp in range(len(blocks)):  # (plans are prepared outside the timed loop)
+        run_staged(blocks[cp]) if world == 1 else run_xchg(blocks[cp])
+    torch.cuda.synchronize(dev)
+    e2e_stream = torch.cuda.current_stream(dev)
 
-    def e2e_step(b):
-        for i, xh in enumerate(host_x):
-            if xh is not None:
-                b[i]["x"].copy_(xh, non_blocking=True)
-        if world == 1:
-            run_staged(b)
-        else:
-            run_xchg(b)
-        for L, yh in zip(b, host_y):
-            yh.copy_(L["y"] if world == 1 else L["g_full"], non_blocking=True)
-        torch.cuda.synchronize(dev)
+    def e2e_step(cp):
+        plan = prepared[("s" if world == 1 else "x", id(blocks[cp]))]
+        plan.run_host(host_x, xbufs[cp], out_views[cp], host_y, stream=e2e_stream)
 
-    e2e_step(blocks[0])
+    e2e_step(0)
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for i in range(e2e_steps):
-        e2e_step(blocks[i % len(blocks)])
+        e2e_step(i % len(blocks))
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
     if world > 1:
@@ -593,11 +623,12 @@ def main():
     e2e = {"value": round(step_bytes * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "ms_per_step": round(e2e_s / e2e_steps * 1e3, 3),
-           "path": "gemm_stages per step (pinned H2D of the step inputs, one staged launch, "
-                   "pinned D2H of all 7 layer outputs, sync)"
-           if world == 1 else "gemm_stages(xchg, comm) per step (pinned H2D of the step inputs, "
-                              "one staged exchange launch, pinned D2H of all 7 gathered outputs, "
-                              "sync)"}
+           "path": "per step: StagedLaunch.run_host (cg_stages_run_host): one pinned H2D of the "
+                   "step inputs (q,k,v x), the prepared staged launch, one pinned D2H of all 7 "
+                   "layer outputs, sync; wall clock"
+           if world == 1 else "per step: StagedLaunch.run_host: one pinned H2D of the step "
+                              "inputs, the prepared staged exchange launch, one pinned D2H of all "
+                              "7 gathered outputs, sync; wall clock, max over ranks"}
 
     base = base_c = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

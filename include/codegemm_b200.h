@@ -74,6 +74,7 @@ extern "C" {
 
 typedef struct cg_layer cg_layer;
 typedef struct cg_comm cg_comm;
+typedef struct cg_stages cg_stages;
 
 #define CG_IPC_HANDLE_BYTES 64 /* cudaIpcMemHandle_t */
 
@@ -205,6 +206,26 @@ int cg_comm_destroy(cg_comm* comm);
 int cg_gemm_stages_xchg(cg_layer* const* layers, const void* const* xs, const int* x_dtypes,
                         float* const* ys, const int* stages, const int* xchg, int count, int n,
                         cg_comm* comm, void* stream);
+
+/*
+ * Prepared staged launch: cg_gemm_stages / cg_gemm_stages_xchg planned once
+ * (task split, shared-memory layout, kernel parameters) for fixed buffers --
+ * a decode loop's per-step call costs one kernel launch.  xchg and comm may
+ * be NULL (no exchange).  The plan is rebuilt automatically if a layer's
+ * split-K workspace was reallocated by a wider call in between.
+ *   cg_stages_launch   : the launch on `stream` (device buffers, asynchronous)
+ *   cg_stages_run_host : end to end with host buffers: x_bytes from x_host to
+ *                        x_dev (the device buffer the plan's inputs live in),
+ *                        the launch, y_bytes from y_dev to y_host, synchronise.
+ *                        Use pinned host memory for asynchronous copies.
+ */
+int cg_stages_prepare(cg_layer* const* layers, const void* const* xs, const int* x_dtypes,
+                      float* const* ys, const int* stages, const int* xchg, int count, int n,
+                      cg_comm* comm, cg_stages** out);
+int cg_stages_launch(cg_stages* plan, void* stream);
+int cg_stages_run_host(cg_stages* plan, const void* x_host, int64_t x_bytes, void* x_dev,
+                       const void* y_dev, void* y_host, int64_t y_bytes, void* stream);
+int cg_stages_destroy(cg_stages* plan);
 
 /* Same with HOST buffers: copies x in, runs, copies y out, synchronises. */
 int cg_layer_gemm_host(cg_layer* layer, const uint16_t* x, int n, float* y, int mode,

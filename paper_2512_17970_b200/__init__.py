@@ -11,6 +11,7 @@ from .engines import (
     DeviceLayer,
     OpCounters,
     Psumbook,
+    StagedLaunch,
     TileConfig,
     build_psumbook,
     closed_form_counters,
@@ -49,7 +50,8 @@ __version__ = "0.1.0"
 __all__ = [
     "BadMagicError", "CodeGemmError", "Codebook", "CodePlane", "ConfigError", "CudaError",
     "DeviceLayer", "DimOverflowError", "FormatError", "IntegrityError", "Matrix", "OpCounters",
-    "Psumbook", "QuantConfig", "QuantizedLayer", "ScalePlane", "ShapeError", "TileConfig",
+    "Psumbook", "QuantConfig", "QuantizedLayer", "ScalePlane", "ShapeError", "StagedLaunch",
+    "TileConfig",
     "TruncatedFileError", "UnsupportedVersionError", "build_psumbook", "closed_form_counters",
     "deserialize", "load_device_layer", "serialize",
     "codegemm_gemm", "encode_f16_array", "gemm_group", "gemm_stages", "pack_codes", "phase_split", "random_layer",

@@ -44,6 +44,10 @@ EXPORTS = (
     "cg_layer_query",
     "cg_gemm_stages",
     "cg_gemm_stages_xchg",
+    "cg_stages_prepare",
+    "cg_stages_launch",
+    "cg_stages_run_host",
+    "cg_stages_destroy",
     "cg_comm_create",
     "cg_comm_buffer",
     "cg_comm_ipc_handle",
@@ -134,6 +138,17 @@ def load() -> ctypes.CDLL:
                                         ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                         i, i, vp, vp]
     lib.cg_gemm_stages_xchg.restype = i
+    lib.cg_stages_prepare.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp),
+                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                      i, i, vp, ctypes.POINTER(vp)]
+    lib.cg_stages_prepare.restype = i
+    lib.cg_stages_launch.argtypes = [vp, vp]
+    lib.cg_stages_launch.restype = i
+    lib.cg_stages_run_host.argtypes = [vp, p, i64, p, p, p, i64, vp]
+    lib.cg_stages_run_host.restype = i
+    lib.cg_stages_destroy.argtypes = [vp]
+    lib.cg_stages_destroy.restype = i
     lib.cg_comm_create.argtypes = [i, i, ctypes.c_int64, i, i, i, ctypes.POINTER(vp)]
     lib.cg_comm_create.restype = i
     lib.cg_comm_buffer.argtypes = [vp, ctypes.POINTER(vp)]

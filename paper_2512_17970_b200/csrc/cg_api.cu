@@ -304,10 +304,17 @@ cg::LayerTask task_of(const cg_layer* L, const uint16_t* x, float* y) {
 
 // One launch of the fused kernel for `count` layers (all fast, same v/m/kbits/device),
 // stages[i] = dependency stage of layer i (non-decreasing; NULL = all stage 0).
-int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const* ys,
-                  const int* stages, int count, int n, cudaStream_t s,
-                  const int* x_dtypes = nullptr, const int* xchg = nullptr,
-                  cg_comm* comm = nullptr) {
+// A planned staged launch: the kernel parameters and launch configuration.
+struct StagedPlan {
+    cg::GroupParams gp;
+    int grid = 0, smem = 0;
+    bool pdl = true;
+    int v = 0, m = 0, u = 0, kbits = 0;
+};
+
+int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const* ys,
+                const int* stages, int count, int n, const int* x_dtypes, const int* xchg,
+                cg_comm* comm, StagedPlan* out) {
     if (count < 1 || count > cg::kMaxGroup)
         return fail(CG_ERR_ARG, "group size %d outside 1..%d", count, cg::kMaxGroup);
     const cg::Plan& p0 = layers[0]->plan;
@@ -532,10 +539,30 @@ int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* con
     if (comm && comm->ctas < layers[0]->sms) gp.flags |= cg::kFlagDbgNoCoop;
     if (layers[0]->flags & CG_OPT_DETERMINISTIC) gp.flags |= cg::kFlagDeterministic;
     if (const char* e = std::getenv("CG_DEBUG_FLAGS")) gp.flags |= std::atoi(e);
-    const bool pdl = !(layers[0]->flags & CG_OPT_NO_PDL) && !(gp.flags & cg::kFlagDbgNoPdl);
-    CG_CUDA(cg::launch_group_gemv(p0.v, p0.m, p0.u, p0.kbits, gp, grid, lay.total, pdl, s),
+    out->gp = gp;
+    out->grid = grid;
+    out->smem = lay.total;
+    out->pdl = !(layers[0]->flags & CG_OPT_NO_PDL) && !(gp.flags & cg::kFlagDbgNoPdl);
+    out->v = p0.v;
+    out->m = p0.m;
+    out->u = p0.u;
+    out->kbits = p0.kbits;
+    return CG_OK;
+}
+
+int launch_plan(const StagedPlan& sp, cudaStream_t s) {
+    CG_CUDA(cg::launch_group_gemv(sp.v, sp.m, sp.u, sp.kbits, sp.gp, sp.grid, sp.smem, sp.pdl, s),
             "fused gemv launch");
     return CG_OK;
+}
+
+int launch_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const* ys,
+                  const int* stages, int count, int n, cudaStream_t s,
+                  const int* x_dtypes = nullptr, const int* xchg = nullptr,
+                  cg_comm* comm = nullptr) {
+    StagedPlan sp;
+    const int rc = plan_stages(layers, xs, ys, stages, count, n, x_dtypes, xchg, comm, &sp);
+    return rc ? rc : launch_plan(sp, s);
 }
 
 // Group launch: layers are partitioned by their tiling u (one kernel
@@ -860,6 +887,99 @@ int cg_gemm_stages_xchg(cg_layer* const* layers, const void* const* xs, const in
     DeviceGuard guard(layers[0]->device);
     return launch_stages(layers, reinterpret_cast<const uint16_t* const*>(xs), ys, stages, count,
                          n, static_cast<cudaStream_t>(stream), x_dtypes, xchg, comm);
+}
+
+// ---- prepared staged launches (cg_stages_*): planned once, launched per call
+struct cg_stages {
+    StagedPlan plan;
+    int count = 0, n = 0, device = 0;
+    cg_layer* layers[cg::kMaxGroup] = {nullptr};
+    const uint16_t* xs[cg::kMaxGroup] = {nullptr};
+    float* ys[cg::kMaxGroup] = {nullptr};
+    int stages[cg::kMaxGroup] = {0}, x_dtypes[cg::kMaxGroup] = {0}, xchg[cg::kMaxGroup] = {0};
+    float* ws[cg::kMaxGroup] = {nullptr};  // split-K workspaces the plan points at
+    cg_comm* comm = nullptr;
+};
+
+namespace {
+int replan_if_needed(cg_stages* P) {
+    bool stale = false;
+    for (int i = 0; i < P->count; ++i) stale |= P->layers[i]->ws != P->ws[i];
+    if (!stale) return CG_OK;  // (a layer's workspace grew for a wider call since)
+    int rc = plan_stages(P->layers, P->xs, P->ys, P->stages, P->count, P->n, P->x_dtypes,
+                         P->comm ? P->xchg : nullptr, P->comm, &P->plan);
+    if (rc) return rc;
+    for (int i = 0; i < P->count; ++i) P->ws[i] = P->layers[i]->ws;
+    return CG_OK;
+}
+}  // namespace
+
+int cg_stages_prepare(cg_layer* const* layers, const void* const* xs, const int* x_dtypes,
+                      float* const* ys, const int* stages, const int* xchg, int count, int n,
+                      cg_comm* comm, cg_stages** out) {
+    if (!out) return fail(CG_ERR_ARG, "NULL out");
+    *out = nullptr;
+    if (!layers || !xs || !ys || !stages) return fail(CG_ERR_ARG, "NULL layers/xs/ys/stages");
+    if (count < 1 || count > cg::kMaxGroup)
+        return fail(CG_ERR_ARG, "launch size %d outside 1..%d", count, cg::kMaxGroup);
+    if (n < 1) return fail(CG_ERR_SHAPE, "x must have >= 1 column, got %d", n);
+    if (xchg && !comm) return fail(CG_ERR_ARG, "xchg flags need a comm");
+    for (int i = 0; i < count; ++i)
+        if (!layers[i] || !xs[i] || !ys[i]) return fail(CG_ERR_ARG, "NULL entry %d", i);
+    DeviceGuard guard(layers[0]->device);
+    cg_stages* P = new cg_stages;
+    P->count = count;
+    P->n = n;
+    P->device = layers[0]->device;
+    P->comm = comm;
+    for (int i = 0; i < count; ++i) {
+        P->layers[i] = layers[i];
+        P->xs[i] = static_cast<const uint16_t*>(xs[i]);
+        P->ys[i] = ys[i];
+        P->stages[i] = stages[i];
+        P->x_dtypes[i] = x_dtypes ? x_dtypes[i] : CG_X_F16;
+        P->xchg[i] = xchg ? xchg[i] : 0;
+    }
+    int rc = plan_stages(P->layers, P->xs, P->ys, P->stages, count, n, P->x_dtypes,
+                         comm ? P->xchg : nullptr, comm, &P->plan);
+    if (rc) {
+        delete P;
+        return rc;
+    }
+    for (int i = 0; i < count; ++i) P->ws[i] = layers[i]->ws;
+    *out = P;
+    return CG_OK;
+}
+
+int cg_stages_launch(cg_stages* P, void* stream) {
+    if (!P) return fail(CG_ERR_ARG, "NULL plan");
+    DeviceGuard guard(P->device);
+    int rc = replan_if_needed(P);
+    return rc ? rc : launch_plan(P->plan, static_cast<cudaStream_t>(stream));
+}
+
+int cg_stages_run_host(cg_stages* P, const void* x_host, int64_t x_bytes, void* x_dev,
+                       const void* y_dev, void* y_host, int64_t y_bytes, void* stream) {
+    if (!P) return fail(CG_ERR_ARG, "NULL plan");
+    if (x_bytes < 0 || y_bytes < 0 || (x_bytes && (!x_host || !x_dev)) ||
+        (y_bytes && (!y_host || !y_dev)))
+        return fail(CG_ERR_ARG, "bad host/device copy arguments");
+    DeviceGuard guard(P->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int rc = replan_if_needed(P);
+    if (rc) return rc;
+    if (x_bytes) CG_CUDA(cudaMemcpyAsync(x_dev, x_host, (size_t)x_bytes, cudaMemcpyHostToDevice, s),
+                         "x H2D");
+    if ((rc = launch_plan(P->plan, s))) return rc;
+    if (y_bytes) CG_CUDA(cudaMemcpyAsync(y_host, y_dev, (size_t)y_bytes, cudaMemcpyDeviceToHost, s),
+                         "y D2H");
+    CG_CUDA(cudaStreamSynchronize(s), "staged host call");
+    return CG_OK;
+}
+
+int cg_stages_destroy(cg_stages* P) {
+    delete P;
+    return CG_OK;
 }
 
 int cg_comm_create(int world, int rank, int64_t bytes, int ctas, int timeout_ms, int device,

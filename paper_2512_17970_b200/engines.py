@@ -268,6 +268,84 @@ def gemm_group(layers, xs, ys=None, stream=None):
     return ys
 
 
+class StagedLaunch:
+    """A prepared staged launch (cg_stages_prepare over cg_gemm_stages / _xchg).
+
+    Planned once for fixed tensors -- as in a decode loop that owns its
+    buffers -- so each call is one kernel launch on the given (default:
+    current) stream; returns the output tensors.  ``run_host`` is the end-to-end
+    form: one host->device copy of the inputs, the launch, one device->host
+    copy of the outputs, synchronise (cg_stages_run_host).
+    """
+
+    def __init__(self, layers, xs, ys, stages, *, xchg=None, comm=None):
+        import torch
+
+        if not layers or not (len(layers) == len(xs) == len(ys) == len(stages)):
+            raise ShapeError("need one x, y and stage per layer")
+        n = int(xs[0].shape[1])
+        for dl, x, y in zip(layers, xs, ys):
+            if (x.dtype not in (torch.float16, torch.float32) or x.dim() != 2
+                    or x.shape[0] != dl.cols or x.shape[1] != n or not x.is_contiguous()):
+                raise ShapeError(f"x for a {dl.rows}x{dl.cols} layer must be contiguous "
+                                 f"({dl.cols}, {n}) float16 or float32")
+            if (y.dtype != torch.float32 or tuple(y.shape) != (dl.rows, n)
+                    or not y.is_contiguous()):
+                raise ShapeError(f"y for a {dl.rows}x{dl.cols} layer must be ({dl.rows}, {n}) "
+                                 "float32")
+        if comm is None and xchg is not None and any(xchg):
+            raise ConfigError("xchg flags need a comm")
+        k = len(layers)
+        if xchg is not None and len(xchg) != k:
+            raise ShapeError("need one xchg flag per layer")
+        self.layers, self.xs, self.ys, self.comm = list(layers), list(xs), list(ys), comm
+        self.device = xs[0].device
+        self._lib = _lib.load()
+        h = ctypes.c_void_p()
+        xf = None if comm is None else (ctypes.c_int * k)(*[int(f) for f in (xchg or [0] * k)])
+        _lib.check(self._lib.cg_stages_prepare(
+            (ctypes.c_void_p * k)(*[dl.handle.value for dl in layers]),
+            (ctypes.c_void_p * k)(*[x.data_ptr() for x in xs]),
+            (ctypes.c_int * k)(*[1 if x.dtype == torch.float32 else 0 for x in xs]),
+            (ctypes.c_void_p * k)(*[y.data_ptr() for y in ys]),
+            (ctypes.c_int * k)(*[int(v) for v in stages]), xf, k, n,
+            None if comm is None else comm.handle, ctypes.byref(h)))
+        self.handle = h
+
+    def _stream(self, stream):
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def __call__(self, stream=None):
+        _lib.check(self._lib.cg_stages_launch(self.handle, self._stream(stream)))
+        return self.ys
+
+    def run_host(self, x_host, x_dev, y_dev, y_host, stream=None):
+        """x_host (pinned CPU) -> x_dev, the launch, y_dev -> y_host (pinned CPU), sync.
+        x_dev / y_dev are device tensors the plan's inputs / outputs live in."""
+        xb = x_host.numel() * x_host.element_size()
+        yb = y_host.numel() * y_host.element_size()
+        if x_dev.numel() * x_dev.element_size() < xb or y_dev.numel() * y_dev.element_size() < yb:
+            raise ShapeError("device buffers smaller than the host copies")
+        _lib.check(self._lib.cg_stages_run_host(self.handle, x_host.data_ptr(), xb,
+                                                x_dev.data_ptr(), y_dev.data_ptr(),
+                                                y_host.data_ptr(), yb, self._stream(stream)))
+        return y_host
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self._lib.cg_stages_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def gemm_stages(layers, xs, ys, stages, stream=None, *, xchg=None, comm=None):
     """One persistent launch running dependent stages of layers (cg_gemm_stages).
 
@@ -285,38 +363,7 @@ def gemm_stages(layers, xs, ys, stages, stream=None, *, xchg=None, comm=None):
     stage) and/or ``dist.XCHG_WAIT`` (x_i is a buffer gathered by an earlier
     launch).
     """
-    import torch
-
-    if not layers or not (len(layers) == len(xs) == len(ys) == len(stages)):
-        raise ShapeError("need one x, y and stage per layer")
-    n = int(xs[0].shape[1])
-    for dl, x, y in zip(layers, xs, ys):
-        if (x.dtype not in (torch.float16, torch.float32) or x.dim() != 2
-                or x.shape[0] != dl.cols or x.shape[1] != n or not x.is_contiguous()):
-            raise ShapeError(f"x for a {dl.rows}x{dl.cols} layer must be contiguous "
-                             f"({dl.cols}, {n}) float16 or float32")
-        if y.dtype != torch.float32 or tuple(y.shape) != (dl.rows, n) or not y.is_contiguous():
-            raise ShapeError(f"y for a {dl.rows}x{dl.cols} layer must be ({dl.rows}, {n}) float32")
-    s = stream if stream is not None else torch.cuda.current_stream(xs[0].device)
-    lib = _lib.load()
-    k = len(layers)
-    hs = (ctypes.c_void_p * k)(*[dl.handle.value for dl in layers])
-    xp = (ctypes.c_void_p * k)(*[x.data_ptr() for x in xs])
-    xd = (ctypes.c_int * k)(*[1 if x.dtype == torch.float32 else 0 for x in xs])
-    yp = (ctypes.c_void_p * k)(*[y.data_ptr() for y in ys])
-    st = (ctypes.c_int * k)(*[int(v) for v in stages])
-    if comm is None:
-        if xchg is not None and any(xchg):
-            raise ConfigError("xchg flags need a comm")
-        _lib.check(lib.cg_gemm_stages(hs, xp, xd, yp, st, k, n, ctypes.c_void_p(s.cuda_stream)))
-        return ys
-    flags = list(xchg) if xchg is not None else [0] * k
-    if len(flags) != k:
-        raise ShapeError("need one xchg flag per layer")
-    xf = (ctypes.c_int * k)(*[int(f) for f in flags])
-    _lib.check(lib.cg_gemm_stages_xchg(hs, xp, xd, yp, st, xf, k, n, comm.handle,
-                                       ctypes.c_void_p(s.cuda_stream)))
-    return ys
+    return StagedLaunch(layers, xs, ys, stages, xchg=xchg, comm=comm)(stream)
 
 
 # one device copy per live layer object (weights are immutable)

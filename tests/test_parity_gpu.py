@@ -395,3 +395,38 @@ def test_staged_chain_m2v8():
                                 q.scales.scales, xin, 8, 128, threads=8)
         assert_within_tolerance(got[i], ref, f"m2v8 stage {i}")
         xin = got[i].astype(np.float16)
+
+
+def test_prepared_staged_launch_and_host_entry():
+    """StagedLaunch (cg_stages_prepare/launch/run_host): bit-identical to
+    gemm_stages in deterministic mode, end to end with pinned host buffers, and
+    re-planned when a wider call reallocated a layer's split-K workspace."""
+    cfg = cg.QuantConfig(v=4, m=1, b=8, g=128)
+    shapes = [(1024, 2048), (2048, 1024), (512, 2048)]
+    layers = _chain(shapes, cfg, 900, u=2, flags=DET)
+    x0 = cuda_x(orc.bench_input_array(2048, 1, 5))
+    ref_ys = [torch.empty((r, 1), dtype=torch.float32, device="cuda") for r, _ in shapes]
+    cg.gemm_stages(layers, [x0] + ref_ys[:-1], ref_ys, [0, 1, 2])
+    ref = [y.cpu().numpy() for y in ref_ys]
+    ybuf = torch.empty(sum(r for r, _ in shapes), dtype=torch.float32, device="cuda")
+    offs = np.cumsum([0] + [r for r, _ in shapes])
+    ys = [ybuf[a:b].view(-1, 1) for a, b in zip(offs, offs[1:])]
+    xdev = torch.empty_like(x0)
+    plan = cg.StagedLaunch(layers, [xdev] + ys[:-1], ys, [0, 1, 2])
+    xdev.copy_(x0)
+    for _ in range(2):
+        ybuf.fill_(float("nan"))
+        plan()
+        for y, r in zip(ys, ref):
+            assert np.array_equal(u32(y.cpu().numpy()), u32(r))
+    host_x = x0.cpu().pin_memory()
+    host_y = torch.empty(ybuf.numel(), dtype=torch.float32).pin_memory()
+    xdev.zero_()
+    plan.run_host(host_x, xdev, ybuf, host_y)
+    assert np.array_equal(u32(host_y.numpy()), u32(np.concatenate(ref).reshape(-1)))
+    # a wider call on the first layer reallocates its workspace: the plan re-plans
+    layers[0].gemm(cuda_x(orc.bench_input_array(2048, 4, 6)))
+    ybuf.fill_(float("nan"))
+    plan()
+    for y, r in zip(ys, ref):
+        assert np.array_equal(u32(y.cpu().numpy()), u32(r))
