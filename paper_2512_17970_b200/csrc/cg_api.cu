@@ -76,7 +76,11 @@ int scale_lg(const cg::Plan& p, int u) {
 // Raw task inputs staged by bulk copy: binary16 codebooks, then (16-byte
 // aligned) the binary16 x slice of one task.
 int raw_books_bytes(const cg::Plan& p) { return (p.m * p.kcount * p.v * 2 + 15) / 16 * 16; }
-int raw_input_bytes(const cg::Plan& p, int u) { return raw_books_bytes(p) + 32 * u * p.v * 2; }
+// raw task-input buffer: codebooks, then the x slice (binary16, or binary32 for a
+// staged-chain input read by bulk copy)
+int raw_input_bytes(const cg::Plan& p, int u, int x_elem_bytes = 2) {
+    return raw_books_bytes(p) + 32 * u * p.v * x_elem_bytes;
+}
 // fix-up list entries (deterministic) or the split-K staging rows (reduce-add)
 int list_bytes_for(int64_t rg_per_task, int n) {
     return (int)std::max((rg_per_task * n + 16) * 16, rg_per_task * 16 * n * 4);
@@ -356,7 +360,7 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
         zmax.psum = std::max(zmax.psum, z.psum);
         zmax.books = std::max(zmax.books, z.books);
         zmax.x = std::max(zmax.x, z.x);
-        raw_bytes = std::max(raw_bytes, raw_input_bytes(p, p.u));
+        raw_bytes = std::max(raw_bytes, raw_input_bytes(p, p.u, (x_dtypes && x_dtypes[i] == CG_X_F32) ? 4 : 2));
         books_raw = std::max(books_raw, raw_books_bytes(p));
         // x travels by bulk copy only if every slice of it is a 16-byte multiple
         if ((reinterpret_cast<uintptr_t>(xs[i]) & 15) || (p.cols % 8)) x_copy = false;

@@ -318,6 +318,14 @@ __device__ __forceinline__ void stage_x_raw(float* xs, const uint16_t* xr, int v
     for (int e = tid; e < S::kSliceSegs * V; e += kThreads)
         xs[x_index<V, M, U, KB>(e / V, e % V)] = e < valid ? h2f(xr[e]) : 0.0f;
 }
+// the same from a binary32 slice (an earlier stage's y), rounded to binary16 as read
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void stage_x_raw32(float* xs, const float* xr, int valid, int tid) {
+    using S = FusedShape<V, M, U, KB>;
+    for (int e = tid; e < S::kSliceSegs * V; e += kThreads)
+        xs[x_index<V, M, U, KB>(e / V, e % V)] =
+            e < valid ? __half2float(__float2half_rn(xr[e])) : 0.0f;
+}
 
 // V binary16 centroid components -> binary32
 template <int V>
@@ -853,8 +861,11 @@ __device__ __forceinline__ bool next_task_s(const CtaState& cs, int nl, int ns, 
     return false;
 }
 
+// x travels by bulk copy (binary16 or binary32) unless several columns or
+// unaligned slices; not for a row-readiness consumer (its x is waited for
+// per row group inside the task, after the copy would have been issued)
 __device__ __forceinline__ bool x_by_copy(const GroupParams& p, const LayerTask& L) {
-    return p.n == 1 && !(p.flags & kFlagXRegs) && L.x32 == nullptr;
+    return p.n == 1 && !(p.flags & kFlagXRegs) && (L.x32 == nullptr || L.dep < 0);
 }
 
 // Task geometry (all task counts fit in 32 bits).
@@ -886,7 +897,8 @@ __device__ __forceinline__ void issue_inputs(const GroupParams& p, TaskCoord c, 
     const uint32_t book_bytes = (uint32_t)((M * L.kcount * V * 2 + 15) & ~15);  // alloc is padded
     const int64_t e0 = (int64_t)g.slice * (S::kSliceSegs * V);
     const int64_t xn = min((int64_t)(S::kSliceSegs * V), L.cols - e0);
-    const uint32_t x_bytes = x_by_copy(p, L) ? (uint32_t)(xn * 2) : 0u;  // host: 16-B multiple
+    const uint32_t x_bytes =
+        x_by_copy(p, L) ? (uint32_t)(xn * (L.x32 ? 4 : 2)) : 0u;  // host: 16-B multiple
     uint64_t* bar = &cs.in_bar[buf];
     unsigned char* raw = smem_raw + p.off_raw[buf];
     if (weights) {
@@ -907,7 +919,10 @@ __device__ __forceinline__ void issue_inputs(const GroupParams& p, TaskCoord c, 
                 prefetch_l2_bulk(base + o, (uint32_t)min(kChunk, bytes - o));
         }
     }
-    if (x && x_bytes) bulk_g2s(raw + p.raw_x_off, L.x + e0, x_bytes, bar);
+    if (x && x_bytes)
+        bulk_g2s(raw + p.raw_x_off,
+                 L.x32 ? static_cast<const void*>(L.x32 + e0) : static_cast<const void*>(L.x + e0),
+                 x_bytes, bar);
 }
 
 template <int V, int M, int U, int KB>
@@ -1001,8 +1016,12 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
         }
         if (x_by_copy(p, L)) {
             const int64_t e0 = (int64_t)slice * (S::kSliceSegs * V);
-            stage_x_raw<V, M, U, KB>(xs, raw + p.raw_x_off / 2,
-                                     (int)min((int64_t)(S::kSliceSegs * V), L.cols - e0), tid);
+            const int valid = (int)min((int64_t)(S::kSliceSegs * V), L.cols - e0);
+            if (L.x32)
+                stage_x_raw32<V, M, U, KB>(
+                    xs, reinterpret_cast<const float*>(raw + p.raw_x_off / 2), valid, tid);
+            else
+                stage_x_raw<V, M, U, KB>(xs, raw + p.raw_x_off / 2, valid, tid);
         } else {
             store_x<V, M, U, KB>(xs, xreg, tid);
         }
@@ -1153,10 +1172,12 @@ __device__ __noinline__ void xc_prologue(const GroupParams& p, CtaState& cs) {
     }
     cs.xc_push_mask = mask;
     cs.xc_layer_mask = lmask;
-    if (wait)
+    if (wait) {
         xc_wait(reinterpret_cast<const unsigned long long*>(p.xc_local + kXcArrive),
                 cs.xc_base * p.xc_world * gridDim.x, (p.flags & kFlagDbgXcGpuScope) != 0,
                 p.xc_timeout_ns);
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // the x copies are TMA reads
+    }
 }
 // all threads, after the grid barrier that closed `stage`: copy this CTA's
 // share of the stage's pushed layers to every peer, release, signal (at the
@@ -1338,6 +1359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_wait();
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 126] = gtimer();
     int stage = 0;
+    if (tid == 0 && p.xc_local) xc_prologue(p, cs);  // (gathered x: wait before it is copied)
     if (tid == 0 && have && cs.l_stage[c.l] == 0)
         issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, false, true);
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 119] = gtimer();
@@ -1347,7 +1369,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                      : "memory");
         cs.l_gen[tid] = gv;
     }
-    if (tid == 0 && p.xc_local) xc_prologue(p, cs);
     if (tid == 32) {  // barrier state (used by thread 0 after the prologue barrier)
         unsigned long long b;
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(b)
