@@ -334,6 +334,25 @@ class StagedLaunch:
                                                 y_host.data_ptr(), yb, self._stream(stream)))
         return y_host
 
+    def bind_host(self, x_host, x_dev, y_dev, y_host, stream=None):
+        """``run_host`` with its arguments bound once: returns a no-argument callable
+        whose each call is one C call (the per-step form for a decode loop)."""
+        xb = x_host.numel() * x_host.element_size()
+        yb = y_host.numel() * y_host.element_size()
+        if x_dev.numel() * x_dev.element_size() < xb or y_dev.numel() * y_dev.element_size() < yb:
+            raise ShapeError("device buffers smaller than the host copies")
+        fn, check = self._lib.cg_stages_run_host, _lib.check
+        args = (self.handle, ctypes.c_void_p(x_host.data_ptr()), ctypes.c_int64(xb),
+                ctypes.c_void_p(x_dev.data_ptr()), ctypes.c_void_p(y_dev.data_ptr()),
+                ctypes.c_void_p(y_host.data_ptr()), ctypes.c_int64(yb), self._stream(stream))
+        keep = (x_host, x_dev, y_dev, y_host)  # the buffers outlive the binding
+
+        def step():
+            check(fn(*args))
+            return keep[3]
+
+        return step
+
     def close(self):
         if getattr(self, "handle", None) is not None and self.handle.value:
             self._lib.cg_stages_destroy(self.handle)

@@ -424,6 +424,10 @@ def test_prepared_staged_launch_and_host_entry():
     xdev.zero_()
     plan.run_host(host_x, xdev, ybuf, host_y)
     assert np.array_equal(u32(host_y.numpy()), u32(np.concatenate(ref).reshape(-1)))
+    host_y.fill_(float("nan"))
+    step = plan.bind_host(host_x, xdev, ybuf, host_y)
+    step()
+    assert np.array_equal(u32(host_y.numpy()), u32(np.concatenate(ref).reshape(-1)))
     # a wider call on the first layer reallocates its workspace: the plan re-plans
     layers[0].gemm(cuda_x(orc.bench_input_array(2048, 4, 6)))
     ybuf.fill_(float("nan"))
