@@ -259,6 +259,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only: the N > 1 code path with every rank on GPU 0 and gloo plumbing
+    # (the fused exchange still runs between the processes over CUDA IPC; the
+    # contexts time-slice, so timings are meaningless; NCCL-only lines skipped)
+    one_gpu = os.environ.get("CG_BENCH_ONE_GPU") == "1" and world > 1
+    if one_gpu:
+        local_rank = 0
     if args.workload == "auto":
         args.workload = "8b" if world == 1 else "70b"
     cfg = CONFIGS[args.config]
@@ -275,7 +281,10 @@ def main():
 
     if world > 1:
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.impl == "reference":
         run_reference(args, spec, cfg, n, rank, world)
         if world > 1:
@@ -474,18 +483,20 @@ def main():
     # ---- the same step with one launch per layer, and one launch per group
     reps = max(20, min(400, args.steps // 4))
     reps = -(-reps // spg) * spg
-    sep = [capture(lambda: [run_layer(L) for b in blocks for L in b])] if world == 1 else \
-        [capture(lambda b=b: [run_layer(L) for L in b]) for b in blocks]
-    timed(sep, 3 * spg, spg)
-    ms_sep = timed(sep, reps, spg) / reps
-    del sep
-    if world == 1:
-        grp = [capture(lambda: [run_group(b, g) for b in blocks for g in groups])]
-    else:  # grouped launches + an NCCL all-gather per layer (the unfused path)
-        grp = [capture(lambda b=b: [run_group(b, g) for g in groups]) for b in blocks]
-    timed(grp, 3 * spg, spg)
-    ms_grp = timed(grp, reps, spg) / reps
-    del grp
+    ms_sep = ms_grp = None
+    if not one_gpu:
+        sep = [capture(lambda: [run_layer(L) for b in blocks for L in b])] if world == 1 else \
+            [capture(lambda b=b: [run_layer(L) for L in b]) for b in blocks]
+        timed(sep, 3 * spg, spg)
+        ms_sep = timed(sep, reps, spg) / reps
+        del sep
+        if world == 1:
+            grp = [capture(lambda: [run_group(b, g) for b in blocks for g in groups])]
+        else:  # grouped launches + an NCCL all-gather per layer (the unfused path)
+            grp = [capture(lambda b=b: [run_group(b, g) for g in groups]) for b in blocks]
+        timed(grp, 3 * spg, spg)
+        ms_grp = timed(grp, reps, spg) / reps
+        del grp
 
     # ---- per-shape kernel microseconds: graphs of R back-to-back launches of
     #      one shape (rotating weight copies), so host launch cost is amortised
@@ -666,13 +677,14 @@ def main():
             "us_per_layer": us_per_layer,
             "us_per_layer_staged_chain": us_chain,
             "us_per_block": round(ms_per_step * 1e3, 3),
-            "step_launches": ([["stage %d: " % s + ",".join(spec[i][0] for i in g)
-                                for s, g in enumerate(groups)]] if world == 1 else
-                              [[spec[i][0] for i in g] for g in groups]),
-            "separate_launches": {"us_per_block": round(ms_sep * 1e3, 3),
+            "step_launches": [["stage %d: " % s + ",".join(spec[i][0] for i in g)
+                               for s, g in enumerate(groups)]],
+            "separate_launches": None if ms_sep is None else
+            {"us_per_block": round(ms_sep * 1e3, 3),
                                   "value": round(step_bytes / (ms_sep / 1e3) / 1e9, 2),
                                   "launches_per_step": len(spec)},
-            "grouped_launches": {"us_per_block": round(ms_grp * 1e3, 3),
+            "grouped_launches": None if ms_grp is None else
+            {"us_per_block": round(ms_grp * 1e3, 3),
                                  "value": round(step_bytes / (ms_grp / 1e3) / 1e9, 2),
                                  "launches_per_step": len(groups),
                                  "all_gather": None if world == 1 else "NCCL, one per layer"},
