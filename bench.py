@@ -408,7 +408,7 @@ def main():
                                             list(STEP_STAGES))
         prepared[key]()
 
-    CHAIN = int(os.environ.get("CG_BENCH_CHAIN", "2"))  # blocks per launch (<= 16 layers)
+    CHAIN = int(os.environ.get("CG_BENCH_CHAIN", "2"))  # blocks per launch (<= 32 layers)
 
     def run_staged_chain(j0):
         """CHAIN block copies, chained, in ONE persistent launch: block j's q,k,v read

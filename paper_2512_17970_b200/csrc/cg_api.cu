@@ -83,7 +83,7 @@ int raw_input_bytes(const cg::Plan& p, int u, int x_elem_bytes = 2) {
 }
 // fix-up list entries (deterministic) or the split-K staging rows (reduce-add)
 int list_bytes_for(int64_t rg_per_task, int n) {
-    return (int)std::max((rg_per_task * n + 16) * 16, rg_per_task * 16 * n * 4);
+    return (int)std::max<int64_t>(std::max((rg_per_task * n + 16) * 16, rg_per_task * 16 * n * 4), 256);
 }
 
 // Planner: pick u (segments per lane) and rows per task for the fused kernel.

@@ -59,7 +59,7 @@ constexpr int kXcFlags = 256;      // u64[16 + kMaxCtas]: this rank's grid-barri
 constexpr int kXcOwnX = 4096;      // u64[kMaxCtas]: exchanges CTA c took part in
 constexpr int kXcHeader = 8192;
 
-constexpr int kMaxGroup = 16;
+constexpr int kMaxGroup = 32;  // layers per launch (kernel parameters ~5 KB: CUDA >= 12.1)
 
 // A launch: up to kMaxGroup layers sharing (v, m, table size) and batch width
 // n, in dependency stages (layers of one stage are independent; a stage may
@@ -135,7 +135,7 @@ inline bool smem_layout(const FusedSizes& z, int scl_bytes, int raw_bytes, int l
                         int reserved, SmemLayout* L, int stage_bytes = 0) {
     auto up = [](int v, int a) { return (v + a - 1) / a * a; };
     const int kMax = 227 * 1024;
-    const int kState = 1024;  // CtaState (incl. the CTA's task list)
+    const int kState = 2048;  // CtaState (incl. the CTA's task list)
     struct Piece {
         int* off;
         int size;

@@ -663,12 +663,13 @@ struct CtaState {
     int xc_elems[kMaxGroup];      // exchange: elements of y per layer (rows * n)
     // row-shard exchange: counts at launch start, exchanges made, stages that push
     unsigned long long xc_base;
-    int xc_n, xc_pushed, xc_push_mask, xc_layer_mask;
+    int xc_n, xc_pushed;
+    unsigned xc_push_mask, xc_layer_mask;  // stages that push, pushed layers (<= 32 each)
     int n_tl;                     // entries (kTaskList = more tasks follow)
     int tl_l[kTaskList], tl_g[kTaskList];
     long long tl_t[kTaskList];
 };
-static_assert(sizeof(CtaState) <= 1024, "CtaState exceeds its shared-memory slot (kState)");
+static_assert(sizeof(CtaState) <= 2048, "CtaState exceeds its shared-memory slot (kState)");
 struct PrevTask {
     int layer;
     long long slice, rg0, rg1;
@@ -1158,13 +1159,13 @@ __device__ __noinline__ void xc_prologue(const GroupParams& p, CtaState& cs) {
     cs.xc_base = own_x[blockIdx.x];
     cs.xc_n = 0;
     cs.xc_pushed = 0;
-    int mask = 0, lmask = 0;
+    unsigned mask = 0, lmask = 0;
     bool wait = false;
     for (int l = 0; l < p.n_layers; ++l) {
         const LayerTask& L = p.layer[l];
         if (L.xchg & kXchgPush) {
-            mask |= 1 << L.stage;
-            lmask |= 1 << l;
+            mask |= 1u << L.stage;
+            lmask |= 1u << l;
         }
         cs.xc_y[l] = L.y;
         cs.xc_elems[l] = (int)(L.rows * p.n);
@@ -1273,7 +1274,7 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
 // this CTA's task list (warp 1, once per launch, beside thread 0's input
 // issue): lane s counts the CTA's tasks in stage s (c, c + grid, ... below the
 // stage's task total), a prefix scan places the stages in the list, and each
-// lane locates list entries k = lane, lane + 32, ...  `scratch` is 48 ints of
+// lane locates list entries k = lane, lane + 32, ...  `scratch` is 64 ints of
 // shared memory that no task uses yet.
 __device__ __forceinline__ void enumerate_tasks(int n_layers, int n_stages, CtaState& cs,
                                                 int* scratch, int lane) {
@@ -1290,15 +1291,13 @@ __device__ __forceinline__ void enumerate_tasks(int n_layers, int n_stages, CtaS
         if (lane >= off) pre += v;
     }
     const int total = __shfl_sync(0xffffffffu, pre, 31);
-    if (lane < kMaxGroup) {
-        scratch[lane] = pre - cnt;  // first list slot of stage `lane`
-        scratch[16 + lane] = cnt;
-    }
+    scratch[lane] = pre - cnt;  // first list slot of stage `lane` (stages <= layers <= 32)
+    scratch[32 + lane] = cnt;
     __syncwarp();
     const int n = min(total, kTaskList);
     for (int k = lane; k < n; k += 32) {
         int s = 0;
-        while (!(k >= scratch[s] && k < scratch[s] + scratch[16 + s])) ++s;
+        while (!(k >= scratch[s] && k < scratch[s] + scratch[32 + s])) ++s;
         TaskCoord e;
         locate_s(cs, n_layers, s, (int64_t)c + (int64_t)(k - scratch[s]) * G, e);
         cs.tl_l[k] = e.l;
