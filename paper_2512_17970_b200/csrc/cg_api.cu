@@ -347,6 +347,9 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
         prev_stage = st;
         int rc = ensure_ws(L, n);
         if (rc) return rc;
+        // the split-K flush is a bulk reduce-add into y: 16-byte aligned rows
+        if (reinterpret_cast<uintptr_t>(ys[i]) & 15)
+            return fail(CG_ERR_ARG, "y of layer %d is not 16-byte aligned", i);
         gp.layer[i] = task_of(L, xs[i], ys[i]);
         gp.layer[i].stage = st;
         if (x_dtypes && x_dtypes[i] == CG_X_F32) {

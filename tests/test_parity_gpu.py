@@ -354,6 +354,15 @@ def test_staged_block_vs_c_oracle():
         assert_within_tolerance(got[i], ref, f"block stage layer {i}")
 
 
+def test_staged_launch_rejects_unaligned_output():
+    q = cg.random_layer(256, 1024, cg.QuantConfig(v=4, m=1, b=8, g=128), seed=31)
+    dl = cg.DeviceLayer(q, u=2)
+    x = cuda_x(orc.bench_input_array(1024, 1, 3))
+    buf = torch.empty(256 + 1, dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError):
+        cg.gemm_stages([dl], [x], [buf[1:].view(256, 1)], [0])
+
+
 def test_staged_launch_rejects_mixed_tiling_and_bad_stages():
     cfg = cg.QuantConfig(v=4, m=1, b=8, g=128)
     a = cg.DeviceLayer(cg.random_layer(256, 1024, cfg, seed=1), u=2)
