@@ -135,7 +135,7 @@ inline bool smem_layout(const FusedSizes& z, int scl_bytes, int raw_bytes, int l
                         int reserved, SmemLayout* L, int stage_bytes = 0) {
     auto up = [](int v, int a) { return (v + a - 1) / a * a; };
     const int kMax = 227 * 1024;
-    const int kState = 2048;  // CtaState (incl. the CTA's task list)
+    const int kState = 3072;  // CtaState (incl. the CTA's task list)
     struct Piece {
         int* off;
         int size;

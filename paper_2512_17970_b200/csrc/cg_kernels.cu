@@ -656,11 +656,12 @@ struct CtaState {
     // this CTA's task list, enumerated once at kernel start (task switches
     // must not walk the layer table: indexed parameter loads are slow)
     int l_stage[kMaxGroup], l_tasks[kMaxGroup];  // per layer, copied from the parameters
-    union {
-        unsigned long long l_gen[kMaxGroup];  // producer layers: completed launches (row deps)
-        float* xc_y[kMaxGroup];               // exchange launches (no row deps): y per layer
-    };
-    int xc_elems[kMaxGroup];      // exchange: elements of y per layer (rows * n)
+    unsigned long long l_gen[kMaxGroup];  // producer layers: completed launches (row deps)
+    // per layer, copied at kernel start by one thread each (loops over the layer
+    // table would be chains of dependent indexed parameter loads, ~0.2 us per layer)
+    float* xc_y[kMaxGroup];       // y
+    int xc_elems[kMaxGroup];      // elements of y (rows * n)
+    int z_per[kMaxGroup];         // elements of y each CTA zeroes (0: not split)
     // row-shard exchange: counts at launch start, exchanges made, stages that push
     unsigned long long xc_base;
     int xc_n, xc_pushed;
@@ -669,7 +670,7 @@ struct CtaState {
     int tl_l[kTaskList], tl_g[kTaskList];
     long long tl_t[kTaskList];
 };
-static_assert(sizeof(CtaState) <= 2048, "CtaState exceeds its shared-memory slot (kState)");
+static_assert(sizeof(CtaState) <= 3072, "CtaState exceeds its shared-memory slot (kState)");
 struct PrevTask {
     int layer;
     long long slice, rg0, rg1;
@@ -941,7 +942,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     const uint16_t* raw = reinterpret_cast<const uint16_t*>(smem_raw + p.off_raw[buf]);
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
     unsigned long long* stamps =
-        (p.stamps && task_idx < 12) ? p.stamps + blockIdx.x * 128 + task_idx * 8 : nullptr;
+        (p.stamps && task_idx < 11) ? p.stamps + blockIdx.x * 128 + task_idx * 8 : nullptr;
 #define CG_STAMP(k) \
     if (stamps && tid == 0) stamps[k] = gtimer();
 
@@ -1167,8 +1168,6 @@ __device__ __noinline__ void xc_prologue(const GroupParams& p, CtaState& cs) {
             mask |= 1u << L.stage;
             lmask |= 1u << l;
         }
-        cs.xc_y[l] = L.y;
-        cs.xc_elems[l] = (int)(L.rows * p.n);
         wait |= (L.xchg & kXchgWait) != 0;
     }
     cs.xc_push_mask = mask;
@@ -1323,16 +1322,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tid = threadIdx.x;
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 124] = gtimer();
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
-    if (tid < p.n_layers) {
-        cs.l_stage[tid] = p.layer[tid].stage;
-        cs.l_tasks[tid] = p.layer[tid].n_tasks;
+    // one layer per warp (lane 0): a warp-uniform parameter index -- per-thread
+    // indices would serialise the constant-cache loads within a warp
+    for (int l = tid >> 5; l < p.n_layers; l += kWarps) {
+        if ((tid & 31) == 0) {
+            const LayerTask& L = p.layer[l];
+            cs.l_stage[l] = L.stage;
+            cs.l_tasks[l] = L.n_tasks;
+            cs.xc_y[l] = L.y;
+            cs.xc_elems[l] = (int)(L.rows * p.n);
+            cs.z_per[l] = L.n_slices > 1 ? L.zero_per : 0;
+        }
     }
     __syncthreads();
-    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 116] = gtimer();
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 88] = gtimer();
     TaskCoord c{0, 0, 0};
     bool have = false;
     for (int s = 0; s < p.n_stages && !have; ++s) have = locate_s(cs, p.n_layers, s, blockIdx.x, c);
-    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 117] = gtimer();
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 89] = gtimer();
     if (tid == 0) {
         mbar_init(&cs.in_bar[0], 1);
         mbar_init(&cs.in_bar[1], 1);
@@ -1347,12 +1354,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // weights of the first task (and its code range into L2) travel
         // before the wait on the previous kernel
         if (have) issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, true, false);
-        if (p.stamps) p.stamps[blockIdx.x * 128 + 118] = gtimer();
+        if (p.stamps) p.stamps[blockIdx.x * 128 + 90] = gtimer();
     }
     if (tid >= 32 && tid < 64) {
         enumerate_tasks(p.n_layers, p.n_stages, cs, reinterpret_cast<int*>(smem_raw + p.off_list),
                         tid & 31);
-        if (p.stamps && tid == 32) p.stamps[blockIdx.x * 128 + 123] = gtimer();
+        if (p.stamps && tid == 32) p.stamps[blockIdx.x * 128 + 91] = gtimer();
     }
     // every layer's x (and y, for write-after-read) belongs to earlier work
     pdl_wait();
@@ -1361,12 +1368,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0 && p.xc_local) xc_prologue(p, cs);  // (gathered x: wait before it is copied)
     if (tid == 0 && have && cs.l_stage[c.l] == 0)
         issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, false, true);
-    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 119] = gtimer();
-    if (tid < p.n_layers && p.layer[tid].rg_cnt) {  // producer generations (row deps)
-        unsigned long long gv;
-        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(gv) : "l"(p.layer[tid].rg_cnt)
-                     : "memory");
-        cs.l_gen[tid] = gv;
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 92] = gtimer();
+    if (p.flags & kFlagRowDeps) {  // producer generations (row deps), one layer per warp
+        for (int l = tid >> 5; l < p.n_layers; l += kWarps) {
+            if ((tid & 31) == 0 && p.layer[l].rg_cnt) {
+                unsigned long long gv;
+                asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(gv) : "l"(p.layer[l].rg_cnt)
+                             : "memory");
+                cs.l_gen[l] = gv;
+            }
+        }
     }
     if (tid == 32) {  // barrier state (used by thread 0 after the prologue barrier)
         unsigned long long b;
@@ -1380,14 +1391,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         // releases its own stores (arrival 1: one unit per warp), so no CTA
         // barrier sits on this path -- the first flush waits for the grid
         bool any = false;
+        const int nl = p.n_layers;
 #pragma unroll 1
-        for (int l = 0; l < p.n_layers; ++l) {
-            const LayerTask& L = p.layer[l];
-            if (L.n_slices <= 1) continue;
+        for (int l = 0; l < nl; ++l) {
+            const int per = cs.z_per[l];
+            if (per == 0) continue;
             any = true;
-            const int elems = (int)(L.rows * p.n), per = L.zero_per;
+            const int elems = cs.xc_elems[l];
             const int e0 = min((int)blockIdx.x * per, elems), e1 = min(e0 + per, elems);
-            float* y = L.y;
+            float* y = cs.xc_y[l];
             // (warps 0 and 1 issue the task inputs and list the tasks meanwhile)
             for (int e = e0 + tid - 64; e < e1 && tid >= 64; e += kThreads - 64) y[e] = 0.0f;
         }
@@ -1398,7 +1410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             cs.zero_pending = 1;
         }
     }
-    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 122] = gtimer();
+    if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 93] = gtimer();
     __syncthreads();  // CTA state (task list, mbarriers) visible to every thread
     bool zero_todo = cs.zero_pending != 0;  // (same in every thread)
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 125] = gtimer();

@@ -81,17 +81,17 @@ def show(name, col):
 
 
 show("kernel entry", st[:, 124])
-show("table copied", st[:, 116])
-show("first task located", st[:, 117])
-show("weights issued", st[:, 118])
-show("before pdl_wait (t0)", st[:, 123])
+show("table copied", st[:, 88])
+show("first task located", st[:, 89])
+show("weights issued", st[:, 90])
+show("before pdl_wait (t0)", st[:, 91])
 show("pdl_wait passed", st[:, 126])
-show("x issued", st[:, 119])
-show("zeroing done (tid 0)", st[:, 122])
+show("x issued", st[:, 92])
+show("zeroing done (tid 0)", st[:, 93])
 show("prologue done", st[:, 125])
 names = [(0, "start"), (7, "synced"), (4, "inputs ok"), (5, "x staged"), (6, "table ready"),
          (1, "gathered"), (2, "zero ok/flush"), (3, "task end")]
-for k in range(12):
+for k in range(11):
     for slot, nm in names:
         if slot in (0, 7, 4, 5, 6, 1, 3):
             show(f"task{k} {nm}", st[:, k * 8 + slot])
