@@ -110,15 +110,17 @@ void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms, int reserved) {
         if (!cg::fused_sizes(p.v, p.m, u, p.kbits, &z)) continue;
         const int n_gs = 32 >> lg;
         const int raw_bytes = raw_input_bytes(p, u);
-        // rows per task are capped by the smem left for the task's scale tiles
+        // rows per task are capped by the smem left for the task's scale tiles;
+        // the cap holds for staged launches too, whose x may be binary32
+        const int raw_cap_bytes = raw_input_bytes(p, u, 4);
         int64_t rg_cap = 0;
         {
             cg::SmemLayout lay;
             int64_t lo = 0, hi = 1 << 16;
             while (lo < hi) {  // largest rg count whose layout fits
                 const int64_t mid = (lo + hi + 1) / 2;
-                if (cg::smem_layout(z, (int)(mid * n_gs * 32), raw_bytes, list_bytes_for(mid, 1),
-                                    reserved, &lay, (int)(mid * 64)))
+                if (cg::smem_layout(z, (int)(mid * n_gs * 32), raw_cap_bytes,
+                                    list_bytes_for(mid, 1), reserved, &lay, (int)(mid * 64)))
                     lo = mid;
                 else hi = mid - 1;
             }

@@ -231,3 +231,21 @@ def test_exchange_two_processes_cuda_ipc():
             raise
     for r, (p, (out, err)) in enumerate(zip(procs, outs)):
         assert p.returncode == 0 and f"OK {r}" in out, out[-2000:] + err[-4000:]
+
+
+def test_exchange_small_grid_caps_rows_per_task():
+    """A comm with few CTAs makes the planner ask for large tasks; rows per task
+    must stay under the shared-memory cap computed for binary32 staged inputs
+    (regression: the cap assumed binary16 x and the launch did not fit)."""
+    qs = [cg.random_layer(r, c, CFG, seed=800 + i)
+          for i, (r, c) in enumerate([(4096, 2048), (2048, 4096)])]
+    x0 = _x0()
+    lay = cgd.GatheredLayout([4096, 2048], 1, 1)
+    comm = cgd.PeerExchange(1, 0, lay.nbytes, ctas=4, timeout_ms=5000)
+    layers = [cg.DeviceLayer(q, u=4, flags=DET) for q in qs]
+    ys = [lay.local(comm, i) for i in range(2)]
+    cg.gemm_stages(layers, [x0, lay.gathered(comm, 0)], ys, [0, 1], xchg=[PUSH] * 2, comm=comm)
+    ref0 = layers[0].gemm(x0)
+    ref1 = layers[1].gemm(ref0.half())
+    assert np.array_equal(u32(ys[0].cpu().numpy()), u32(ref0.cpu().numpy()))
+    assert np.array_equal(u32(ys[1].cpu().numpy()), u32(ref1.cpu().numpy()))
