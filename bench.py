@@ -408,7 +408,7 @@ def main():
                                             list(STEP_STAGES))
         prepared[key]()
 
-    CHAIN = int(os.environ.get("CG_BENCH_CHAIN", "2"))  # blocks per launch (<= 32 layers)
+    CHAIN = int(os.environ.get("CG_BENCH_CHAIN", "2"))  # blocks per launch (<= 16 layers)
 
     def run_staged_chain(j0):
         """CHAIN block copies, chained, in ONE persistent launch: block j's q,k,v read
@@ -485,17 +485,20 @@ def main():
     reps = -(-reps // spg) * spg
     ms_sep = ms_grp = None
     if not one_gpu:
+        # (N=1: one graph over every block copy -- `nb` steps per replay)
+        nb = len(blocks) if world == 1 else 1
+        reps_nb = -(-reps // nb) * nb
         sep = [capture(lambda: [run_layer(L) for b in blocks for L in b])] if world == 1 else \
             [capture(lambda b=b: [run_layer(L) for L in b]) for b in blocks]
-        timed(sep, 3 * spg, spg)
-        ms_sep = timed(sep, reps, spg) / reps
+        timed(sep, 3 * nb, nb)
+        ms_sep = timed(sep, reps_nb, nb) / reps_nb
         del sep
         if world == 1:
             grp = [capture(lambda: [run_group(b, g) for b in blocks for g in groups])]
         else:  # grouped launches + an NCCL all-gather per layer (the unfused path)
             grp = [capture(lambda b=b: [run_group(b, g) for g in groups]) for b in blocks]
-        timed(grp, 3 * spg, spg)
-        ms_grp = timed(grp, reps, spg) / reps
+        timed(grp, 3 * nb, nb)
+        ms_grp = timed(grp, reps_nb, nb) / reps_nb
         del grp
 
     # ---- per-shape kernel microseconds: graphs of R back-to-back launches of

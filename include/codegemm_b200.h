@@ -145,7 +145,7 @@ int cg_layer_query(const cg_layer* layer, cg_layer_info* info);
 int cg_layer_gemm(cg_layer* layer, const void* x, int n, float* y, int mode, void* stream);
 
 /*
- * Grouped launch: y_i = W_i x_i for `count` (1..32) independent layers in ONE
+ * Grouped launch: y_i = W_i x_i for `count` (1..16) independent layers in ONE
  * launch of the fused kernel (e.g. the q/k/v or gate/up projections of a
  * decoder block, which read the same x).  Layers must share v, m, the code
  * width class (b <= 4 or b <= 8) and the device, and must all have
@@ -157,7 +157,7 @@ int cg_gemm_group(cg_layer* const* layers, const void* const* xs, float* const* 
 
 /*
  * Dependency-staged launch: one persistent launch of the fused kernel runs
- * `count` (1..32) layers in stages; stages[i] is layer i's stage (starts at 0,
+ * `count` (1..16) layers in stages; stages[i] is layer i's stage (starts at 0,
  * non-decreasing, steps of at most 1).  Layers of one stage are independent
  * (a grouped launch); a stage may read what earlier stages wrote -- e.g. a
  * decoder-block chain {q} -> {o} -> {gate,up} -> {down}.  x_dtypes[i] (NULL =

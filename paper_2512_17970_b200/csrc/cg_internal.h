@@ -59,7 +59,7 @@ constexpr int kXcFlags = 256;      // u64[16 + kMaxCtas]: this rank's grid-barri
 constexpr int kXcOwnX = 4096;      // u64[kMaxCtas]: exchanges CTA c took part in
 constexpr int kXcHeader = 8192;
 
-constexpr int kMaxGroup = 32;  // layers per launch (kernel parameters ~5 KB: CUDA >= 12.1)
+constexpr int kMaxGroup = 16;  // layers per launch (kernel parameters ~2.7 KB)
 
 // A launch: up to kMaxGroup layers sharing (v, m, table size) and batch width
 // n, in dependency stages (layers of one stage are independent; a stage may
