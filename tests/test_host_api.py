@@ -127,3 +127,10 @@ def test_gemm_stages_argument_checks():
         cg.gemm_stages([a], [x], [ya.to(torch.float16)], [0])
     with pytest.raises(cg.ShapeError):
         cg.gemm_stages([a], [x], [yb], [0])
+    # prepared launches check the same, plus the exchange arguments
+    with pytest.raises(cg.ShapeError):
+        cg.StagedLaunch([a, b], [x], [ya, yb], [0, 1])
+    with pytest.raises(cg.ConfigError):  # exchange flags without a comm
+        cg.StagedLaunch([a], [x], [ya], [0], xchg=[1])
+    with pytest.raises(cg.ShapeError):  # one flag per layer
+        cg.StagedLaunch([a], [x], [ya], [0], xchg=[1, 1], comm=object())
