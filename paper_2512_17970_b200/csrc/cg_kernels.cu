@@ -1215,10 +1215,12 @@ __device__ __noinline__ void xc_push(unsigned char* smem_raw, int off_bar, int s
     __syncthreads();
 }
 
-// Grid barrier between dependent stages of a launch (sense reversal on
-// {count, generation}).  Everything this CTA wrote in the stage -- plain
-// stores and the bulk (async-proxy) reduce-adds -- is complete and released
-// before the arrival; the next stage's x, read by TMA, is acquired after.
+// Grid barrier between dependent stages of a launch (the monotonic counter
+// above).  Everything this CTA wrote in the stage -- plain stores and the bulk
+// (async-proxy) reduce-adds -- is complete and released before the arrival;
+// the next stage's x, read by TMA, is acquired after.  In an exchange launch
+// the stage's rows then go to the peers (and, unless `final`, every rank's
+// rows are awaited).
 __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned char* smem_raw,
                                               int tid, int stage, bool final = false) {
     __syncthreads();
@@ -1226,19 +1228,18 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
     unsigned long long* st =
         (p.stamps && cs.n_bar < 7) ? p.stamps + blockIdx.x * 128 + 96 + 4 * cs.n_bar : nullptr;
-    const bool first_bar = true;  // (stamps of the first three barriers)
     if (tid == 0) {
-        if (st && first_bar) st[0] = gtimer();
+        if (st) st[0] = gtimer();
         cs.prev_layer = -1;
         bulk_wait_all();
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        if (st && first_bar) st[1] = gtimer();
+        if (st) st[1] = gtimer();
         ++cs.n_arrive;
         grid_red(p, kBarUnits);
-        if (st && first_bar) st[2] = gtimer();
+        if (st) st[2] = gtimer();
         grid_wait(p, cs, cs.n_arrive);
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        if (st && first_bar) st[3] = gtimer();
+        if (st) st[3] = gtimer();
         ++cs.n_bar;
     }
     __syncthreads();
@@ -1322,8 +1323,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tid = threadIdx.x;
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 124] = gtimer();
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
-    // one layer per warp (lane 0): a warp-uniform parameter index -- per-thread
-    // indices would serialise the constant-cache loads within a warp
+    // the layer table's per-layer fields into shared memory, one layer per warp
+    // (lane 0): later loops over the layers read shared memory only
     for (int l = tid >> 5; l < p.n_layers; l += kWarps) {
         if ((tid & 31) == 0) {
             const LayerTask& L = p.layer[l];
