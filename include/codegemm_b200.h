@@ -149,8 +149,10 @@ int cg_layer_gemm(cg_layer* layer, const void* x, int n, float* y, int mode, voi
  * launch of the fused kernel (e.g. the q/k/v or gate/up projections of a
  * decoder block, which read the same x).  Layers must share v, m, the code
  * width class (b <= 4 or b <= 8) and the device, and must all have
- * fast_supported.  Device buffers, n columns each, stream-ordered.  Outputs
- * are bit-identical to separate cg_layer_gemm calls (CG_MODE_FAST).
+ * fast_supported.  Device buffers, n columns each, stream-ordered.  With
+ * CG_OPT_DETERMINISTIC layers the outputs are bit-identical to separate
+ * cg_layer_gemm calls (CG_MODE_FAST); without it split-K partials are added in
+ * L2 in arrival order (within the fast-mode tolerance, not bit-reproducible).
  */
 int cg_gemm_group(cg_layer* const* layers, const void* const* xs, float* const* ys, int count,
                   int n, void* stream);
@@ -167,8 +169,11 @@ int cg_gemm_group(cg_layer* const* layers, const void* const* xs, float* const* 
  * reference's fp16 boundary rounding (cli.py:136).  The kernel's grid barrier
  * orders a stage's reads after the earlier stages' writes.  Same layer
  * requirements as cg_gemm_group, plus one tiling u for all layers
- * (cg_layer_options.u).  Outputs are bit-identical to separate cg_layer_gemm
- * calls in stage order on the rounded inputs.
+ * (cg_layer_options.u).  With CG_OPT_DETERMINISTIC layers the outputs are
+ * bit-identical to separate cg_layer_gemm calls in stage order on the rounded
+ * inputs.  An x may overlap only the y of an EARLIER stage: a y written in the
+ * same or a later stage is rejected (CG_ERR_ARG) -- split-K outputs are zeroed
+ * by every CTA when the launch starts, before stage 0 reads its x.
  */
 int cg_gemm_stages(cg_layer* const* layers, const void* const* xs, const int* x_dtypes,
                    float* const* ys, const int* stages, int count, int n, void* stream);
@@ -251,6 +256,14 @@ int cg_layer_unpack_codes(cg_layer* layer, uint16_t* out, void* stream);
  */
 int cg_psumbook_build(const void* books, const void* x, int m, int b, int v, int64_t k_len,
                       int n, float* out, void* stream);
+/*
+ * The same from binary32 books and x (engines.py:137-156 widens any float
+ * input to binary32): each entry is ((0 + c0*x0) + c1*x1) + ... with every
+ * product and sum rounded separately, as numpy does -- bit-exact for inputs
+ * that are not binary16-representable too.
+ */
+int cg_psumbook_build_f32(const float* books, const float* x, int m, int b, int v, int64_t k_len,
+                          int n, float* out, void* stream);
 
 #ifdef __cplusplus
 }

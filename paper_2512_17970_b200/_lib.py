@@ -169,6 +169,8 @@ def load() -> ctypes.CDLL:
     lib.cg_layer_unpack_codes.restype = i
     lib.cg_psumbook_build.argtypes = [p, p, i, i, i, i64, i, p, vp]
     lib.cg_psumbook_build.restype = i
+    lib.cg_psumbook_build_f32.argtypes = [p, p, i, i, i, i64, i, p, vp]
+    lib.cg_psumbook_build_f32.restype = i
     _lib = lib
     return lib
 

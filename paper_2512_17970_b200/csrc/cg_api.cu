@@ -68,9 +68,9 @@ int scale_lg(const cg::Plan& p, int u) {
     if (p.g_eff % lane_elems != 0 || slice_elems % p.g_eff != 0) return -1;
     const int64_t lanes = p.g_eff / lane_elems;
     if (!pow2(lanes)) return -1;
-    // the gather applies scales once 8 lanes are summed (branch-free
-    // reduction): a scale group must span >= 8 lanes
-    return lanes >= 8 ? ilog2(lanes) : -1;
+    // >= 8 lanes: the gather scales two slots after three halvings; 1, 2 or 4
+    // lanes: all 16 slots of a lane before the reduction
+    return ilog2(lanes);
 }
 
 // Raw task inputs staged by bulk copy: binary16 codebooks, then (16-byte
@@ -272,6 +272,7 @@ int ensure_ws(cg_layer* L, int n) {
         L->device_bytes -= (int64_t)p.n_slices * p.rows * L->ws_cols * 4 + p.n_rg * L->ws_cols * 8;
         L->ws = nullptr;
         L->tickets = nullptr;
+        L->ws_cols = 0;  // (a failed reallocation below must not leave a stale width)
     }
     int rc = dev_alloc(L, &L->ws, (size_t)p.n_slices * p.rows * n * 4, "workspace alloc");
     if (rc) return rc;
@@ -371,6 +372,23 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
         if ((reinterpret_cast<uintptr_t>(xs[i]) & 15) || (p.cols % 8)) x_copy = false;
     }
     gp.n_stages = prev_stage + 1;
+    // An x must not overlap a y written in its own stage or later: split-K outputs
+    // are zeroed by every CTA at launch start (before stage 0 reads its x) and a
+    // same-stage y is written while x is read.  Only an earlier stage's y may be
+    // read (the staged chain).
+    for (int i = 0; i < count; ++i) {
+        const int64_t xe = (x_dtypes && x_dtypes[i] == CG_X_F32) ? 4 : 2;
+        const uintptr_t x0 = reinterpret_cast<uintptr_t>(xs[i]);
+        const uintptr_t x1 = x0 + (uintptr_t)(layers[i]->plan.cols * n * xe);
+        for (int j = 0; j < count; ++j) {
+            const uintptr_t y0 = reinterpret_cast<uintptr_t>(ys[j]);
+            const uintptr_t y1 = y0 + (uintptr_t)(layers[j]->plan.rows * n * 4);
+            if (x0 < y1 && y0 < x1 && gp.layer[j].stage >= gp.layer[i].stage)
+                return fail(CG_ERR_ARG,
+                            "x of layer %d overlaps y of layer %d, which is written in the same or "
+                            "a later stage (outputs are zeroed at launch start)", i, j);
+        }
+    }
     // ---- row-shard exchange: pushed y / gathered x must lie in the comm region
     if (comm) {
         if (!comm->linked) return fail(CG_ERR_ARG, "comm peers not opened / set");
@@ -1104,6 +1122,7 @@ int cg_layer_gemm_host(cg_layer* L, const uint16_t* x, int n, float* y, int mode
         L->y_dev = nullptr;
         L->x_pin = nullptr;
         L->y_pin = nullptr;
+        L->stage_cols = 0;  // (a failed reallocation below must not leave a stale width)
         CG_CUDA(cudaMalloc(&L->x_dev, xb), "x staging alloc");
         CG_CUDA(cudaMalloc(&L->y_dev, yb), "y staging alloc");
         CG_CUDA(cudaHostAlloc(&L->x_pin, xb, cudaHostAllocDefault), "pinned x alloc");
@@ -1162,6 +1181,22 @@ int cg_psumbook_build(const void* books, const void* x, int m, int b, int v, int
     CG_CUDA(cg::launch_psumbook_build(static_cast<const uint16_t*>(books),
                                       static_cast<const uint16_t*>(x), m, b, v, k_len, n, out,
                                       static_cast<cudaStream_t>(stream)),
+            "psumbook build launch");
+    return CG_OK;
+}
+
+int cg_psumbook_build_f32(const float* books, const float* x, int m, int b, int v, int64_t k_len,
+                          int n, float* out, void* stream) {
+    if (!books || !x || !out) return fail(CG_ERR_ARG, "NULL books/x/out");
+    if (m < 1 || v < 1 || b < 1 || b > 16) return fail(CG_ERR_CONFIG, "bad m/v/b");
+    if (k_len < 1 || k_len % v)
+        return fail(CG_ERR_CONFIG, "tile width %lld not divisible by v=%d", (long long)k_len, v);
+    if (n < 1) return fail(CG_ERR_SHAPE, "n must be >= 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(CG_ERR_CUDA, "no CUDA device available; this library has no CPU path");
+    CG_CUDA(cg::launch_psumbook_build_f32(books, x, m, b, v, k_len, n, out,
+                                          static_cast<cudaStream_t>(stream)),
             "psumbook build launch");
     return CG_OK;
 }

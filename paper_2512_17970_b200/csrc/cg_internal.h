@@ -217,6 +217,8 @@ cudaError_t launch_unpack_packed(const uint8_t* packed, int64_t plane_bytes, int
                                  int64_t per_plane, int b, uint16_t* out, cudaStream_t s);
 cudaError_t launch_psumbook_build(const uint16_t* books, const uint16_t* x, int m, int b, int v,
                                   int64_t k_len, int n, float* out, cudaStream_t s);
+cudaError_t launch_psumbook_build_f32(const float* books, const float* x, int m, int b, int v,
+                                      int64_t k_len, int n, float* out, cudaStream_t s);
 
 
 

@@ -565,7 +565,8 @@ __device__ __forceinline__ void load_tile(uint4 (&cw)[M][U], const uint8_t* tp) 
 // the LDS immediate: one PRMT + one LDS per lookup, no address arithmetic.
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ float gather_row_group(const uint4 (&cw)[M][U], const uint16_t* sp,
-                                                  uint32_t lb0, uint32_t lb1, int mask) {
+                                                  uint32_t lb0, uint32_t lb1, int mask,
+                                                  bool early) {
     using S = FusedShape<V, M, U, KB>;
     // lookups: a[i] = sum over (t, u) of psum_t[seg(lane,u)][code of slot i],
     // two slots at a time with packed FADD2
@@ -597,15 +598,19 @@ __device__ __forceinline__ float gather_row_group(const uint4 (&cw)[M][U], const
         a[i + 1] = s2.y;
     }
     // Transpose-reduce the 16 slot partials across lanes; lanes 0-15 keep their
-    // rows' sums.  The fused kernel requires a scale group to span >= 8 lanes
-    // (lg >= 3; every g = 128 configuration), so after the first
-    // three halvings (lanes differing in bits 0-2 summed) all lanes still to
-    // be combined share each row's scale: the scales are applied there, to the
-    // two remaining slots, and the reduction is branch-free.
+    // rows' sums.  When a scale group spans >= 8 lanes (lg >= 3; every g = 128
+    // configuration), after the first three halvings (lanes
+    // differing in bits 0-2 summed) all lanes still to be combined share each
+    // row's scale: the scales are applied there, to the two remaining slots.
+    // Smaller groups (g = v, 2v, 32 ... : 1, 2 or 4 lanes per group, `early`)
+    // scale all 16 slots of the lane before the first halving -- the
+    // reference's per-segment scale (engines.py:294) applied per lane.
+    // `sp` is the lane's group tile (16 rows, row order).
+    if (early) apply_scales<16>(a, sp, mask);
     halve<16>(a, 1);
     halve<8>(a, 2);
     halve<4>(a, 4);
-    apply_scales<2>(a, sp, mask & 1);
+    if (!early) apply_scales<2>(a, sp + (mask & ~1), mask & 1);
     halve<2>(a, 8);
     a[0] += __shfl_xor_sync(0xffffffffu, a[0], 16);
     return a[0];
@@ -997,11 +1002,11 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     if (psum_addr & 0xffffu) __trap();
     const uint32_t lb0 = ((uint32_t)lane << 2) | ((psum_addr >> 16) << 8);
     const uint32_t lb1 = lb0 | 0x80u;
-    const int lg = L.lg;  // >= 3 (host planner)
+    const int lg = L.lg;  // lanes per scale group = 2**lg (host planner)
+    const bool early = lg < 3;  // scales applied per lane (small groups)
     const int mask = row_mask(lane);
-    const int sbase = mask & ~1;  // first row of this lane's two scaled slots
     const int gi = lg >= 5 ? 0 : (lane >> lg);
-    const uint16_t* sp0 = scl_s + (warp * n_gs + gi) * 16 + sbase;
+    const uint16_t* sp0 = scl_s + (warp * n_gs + gi) * 16;
     const int sstep = kWarps * n_gs * 16;
     // split-K partials: staged in smem and flushed by one bulk reduce-add per
     // task (one column), or -- several columns -- added straight into y with
@@ -1062,7 +1067,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
                     if (pf > 0 && lane == 0 && i + pf < load_rgs)
                         prefetch_l2_bulk(cptr - lane * 16 + (i + pf) * kStep, S::kTileBytes);
                     const float v = gather_row_group<V, M, U, KB>(tb[d], sp0 + i * sstep, lb0, lb1,
-                                                                  mask);
+                                                                  mask, early);
                     if (i + D < load_rgs) load_tile<V, M, U, KB>(tb[d], cptr + (i + D) * kStep);
                     if (lane < 16 && row < L.rows) {
                         if (direct) atomicAdd(out + row * n + col, v);  // (RED, result unused)
@@ -1569,6 +1574,28 @@ __global__ void psumbook_build_kernel(const uint16_t* __restrict__ books,
     }
 }
 
+// K1 from binary32 inputs (engines.py:137-156 widens any float tile/book to
+// binary32): products and sums rounded separately, as numpy's multiply + add
+// (engines.py:126-133) -- with binary32 operands a product is not exact, so
+// no fma here
+__global__ void psumbook_build_f32_kernel(const float* __restrict__ books,
+                                          const float* __restrict__ x, float* __restrict__ out,
+                                          int m, int kcount, int v, int64_t segs, int n) {
+    const int64_t total = (int64_t)m * segs * kcount * n;
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
+         o += (int64_t)gridDim.x * blockDim.x) {
+        const int col = (int)(o % n);
+        const int64_t i = (o / n) % kcount;
+        const int64_t seg = (o / ((int64_t)n * kcount)) % segs;
+        const int64_t t = o / ((int64_t)n * kcount * segs);
+        const float* c = books + (t * kcount + i) * v;
+        float acc = 0.0f;
+        for (int k = 0; k < v; ++k)
+            acc = __fadd_rn(acc, __fmul_rn(c[k], x[(seg * v + k) * (int64_t)n + col]));
+        out[o] = acc;
+    }
+}
+
 int grid_for(int64_t total, int threads) {
     int64_t blocks = (total + threads - 1) / threads;
     if (blocks > 148 * 32) blocks = 148 * 32;
@@ -1785,6 +1812,16 @@ cudaError_t launch_psumbook_build(const uint16_t* books, const uint16_t* x, int 
     const int64_t total = (int64_t)m * segs * kcount * n;
     psumbook_build_kernel<<<grid_for(total, 256), 256, 0, s>>>(books, x, out, m, kcount, v, segs,
                                                                n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_psumbook_build_f32(const float* books, const float* x, int m, int b, int v,
+                                      int64_t k_len, int n, float* out, cudaStream_t s) {
+    const int kcount = 1 << b;
+    const int64_t segs = k_len / v;
+    const int64_t total = (int64_t)m * segs * kcount * n;
+    psumbook_build_f32_kernel<<<grid_for(total, 256), 256, 0, s>>>(books, x, out, m, kcount, v,
+                                                                   segs, n);
     return cudaGetLastError();
 }
 

@@ -27,6 +27,7 @@ are independent of both, engines.py:15-22).
 from __future__ import annotations
 
 import ctypes
+import warnings
 import weakref
 from dataclasses import dataclass
 from fractions import Fraction
@@ -119,6 +120,29 @@ def _layer_arrays(q):
     return codes, books, scales
 
 
+class StrictFallbackWarning(RuntimeWarning):
+    """mode="auto" on a layer without a fused kernel: the strict kernel (one thread
+    per output, serial over K -- tens of times slower) runs instead."""
+
+
+def _warn_if_strict(dl, mode: str) -> None:
+    if mode == "auto" and not dl.info["fast_supported"]:
+        warnings.warn(
+            f"no fused kernel for v={dl.v} m={dl.m} b={dl.b} g={dl.g} (cols={dl.cols}); "
+            "mode='auto' runs the strict kernel (reference operation order, one thread per "
+            "output) -- pass mode='strict' to silence this", StrictFallbackWarning, stacklevel=3)
+
+
+def _check_y(y, rows: int, n: int, device) -> None:
+    """A caller-supplied output must be a contiguous float32 (rows, n) tensor on x's device."""
+    import torch
+
+    if (y.dtype != torch.float32 or tuple(y.shape) != (rows, n) or not y.is_contiguous()
+            or y.device != device):
+        raise ShapeError(f"y must be a contiguous float32 ({rows}, {n}) tensor on {device}, got "
+                         f"{tuple(y.shape)} {y.dtype} on {y.device}")
+
+
 class DeviceLayer:
     """A quantized layer uploaded, prepacked and resident on one B200.
 
@@ -193,6 +217,7 @@ class DeviceLayer:
             raise ShapeError(f"layer is {self.rows}x{self.cols} but X is {x.shape}")
         n = int(x.shape[1])
         y = np.empty((self.rows, n), dtype=np.float32)
+        _warn_if_strict(self, mode)
         _lib.check(self._lib.cg_layer_gemm_host(self._handle, x.ctypes.data, n, y.ctypes.data,
                                                 _lib.MODES[mode], None))
         return y
@@ -209,6 +234,9 @@ class DeviceLayer:
         n = int(x.shape[1])
         if y is None:
             y = torch.empty((self.rows, n), dtype=torch.float32, device=x.device)
+        else:
+            _check_y(y, self.rows, n, x.device)
+        _warn_if_strict(self, mode)
         s = stream if stream is not None else torch.cuda.current_stream(x.device)
         _lib.check(self._lib.cg_layer_gemm(self._handle, x.data_ptr(), n, y.data_ptr(),
                                            _lib.MODES[mode], ctypes.c_void_p(s.cuda_stream)))
@@ -218,6 +246,9 @@ class DeviceLayer:
         """The fused kernel's shared-memory Psumbook, (m, cols/v, 2**b, n) float32."""
         import torch
 
+        if x.dtype != torch.float16 or not x.is_cuda or x.dim() != 2 or x.shape[0] != self.cols:
+            raise ShapeError(f"x must be a CUDA float16 ({self.cols}, n) tensor, got "
+                             f"{tuple(x.shape)} {x.dtype}")
         x = x.contiguous()
         n = int(x.shape[1])
         out = torch.empty((self.m, self.cols // self.v, 1 << self.b, n), dtype=torch.float32,
@@ -244,7 +275,9 @@ def gemm_group(layers, xs, ys=None, stream=None):
 
     ``layers``: DeviceLayer objects sharing v, m and code width; ``xs``: CUDA
     float16 (cols_i, n) tensors with the same n; returns the (rows_i, n)
-    float32 outputs, bit-identical to calling ``gemm`` on each layer.
+    float32 outputs -- bit-identical to calling ``gemm`` on each layer when the
+    layers were created with ``CG_OPT_DETERMINISTIC`` (otherwise split-K partials
+    are added in L2 in arrival order, within the fast-mode tolerance).
     """
     import torch
 
@@ -253,11 +286,17 @@ def gemm_group(layers, xs, ys=None, stream=None):
     n = int(xs[0].shape[1])
     xs = [x.contiguous() for x in xs]
     for dl, x in zip(layers, xs):
-        if x.dtype != torch.float16 or x.dim() != 2 or x.shape[0] != dl.cols or x.shape[1] != n:
+        if (x.dtype != torch.float16 or not x.is_cuda or x.dim() != 2 or x.shape[0] != dl.cols
+                or x.shape[1] != n):
             raise ShapeError(f"x for a {dl.rows}x{dl.cols} layer must be ({dl.cols}, {n}) float16")
     if ys is None:
         ys = [torch.empty((dl.rows, n), dtype=torch.float32, device=x.device)
               for dl, x in zip(layers, xs)]
+    else:
+        if len(ys) != len(layers):
+            raise ShapeError("need one y per layer")
+        for dl, x, y in zip(layers, xs, ys):
+            _check_y(y, dl.rows, n, x.device)
     s = stream if stream is not None else torch.cuda.current_stream(xs[0].device)
     lib = _lib.load()
     k = len(layers)
@@ -345,11 +384,15 @@ class StagedLaunch:
         args = (self.handle, ctypes.c_void_p(x_host.data_ptr()), ctypes.c_int64(xb),
                 ctypes.c_void_p(x_dev.data_ptr()), ctypes.c_void_p(y_dev.data_ptr()),
                 ctypes.c_void_p(y_host.data_ptr()), ctypes.c_int64(yb), self._stream(stream))
-        keep = (x_host, x_dev, y_dev, y_host)  # the buffers outlive the binding
+        # the plan (its C handle) and the buffers outlive the binding; a closed
+        # plan invalidates it (the handle is checked on every call)
+        keep = (self, x_host, x_dev, y_dev, y_host)
 
         def step():
+            if not keep[0].handle or not keep[0].handle.value:
+                raise ConfigError("the StagedLaunch behind this bound step was closed")
             check(fn(*args))
-            return keep[3]
+            return keep[4]
 
         return step
 
@@ -390,11 +433,15 @@ _CACHE: dict = {}
 
 
 def device_layer_for(q) -> DeviceLayer:
+    """The cached device copy behind ``codegemm_gemm``.  Created with
+    CG_OPT_DETERMINISTIC: like the reference (engines.py:15-22, 255-257) the
+    drop-in's output bits do not change from run to run or with the tiling --
+    split-K partials are summed in a fixed order instead of added in L2."""
     key = id(q)
     hit = _CACHE.get(key)
     if hit is not None and hit[0]() is q:
         return hit[1]
-    dl = DeviceLayer(q)
+    dl = DeviceLayer(q, flags=_lib.CG_OPT_DETERMINISTIC)
     try:
         ref = weakref.ref(q, lambda _r, k=key: _CACHE.pop(k, None))
     except TypeError:  # not weak-referenceable: keep the layer alive instead
@@ -438,30 +485,39 @@ def codegemm_gemm(q, x, tiles: TileConfig | None = None, threads: int = 1, *,
 
 
 def build_psumbook(x_tile, books, counters=None) -> Psumbook:
-    """Psumbook of one input column on the GPU (engines.py:137-156), bit-exact."""
+    """Psumbook of one input column on the GPU (engines.py:137-156), bit-exact.
+
+    As in the reference, the tile (any float dtype) and the codebooks (Codebook
+    objects or raw arrays) are widened to binary32 and every entry is
+    ((0 + c0*x0) + c1*x1) + ... with separately rounded products and sums
+    (cg_psumbook_build_f32) -- bit-exact also for inputs that are not
+    binary16-representable.
+    """
     import torch
 
+    x32 = np.asarray(x_tile, dtype=np.float32).reshape(-1)
     books = list(books)
     if not books:
         raise ConfigError("at least one codebook required")
-    ents = [np.asarray(getattr(bk, "entries", bk)) for bk in books]
+    ents = [np.asarray(bk.entries if hasattr(bk, "entries") else bk, dtype=np.float32)
+            for bk in books]
     v = int(ents[0].shape[1])
-    x16 = np.asarray(x_tile, dtype=np.float16).reshape(-1)
-    if x16.size == 0 or x16.size % v:
-        raise ConfigError(f"tile width {x16.size} not divisible by v={v}")
+    if x32.size == 0 or x32.size % v:
+        raise ConfigError(f"tile width {x32.size} not divisible by v={v}")
     k = int(ents[0].shape[0])
     b = k.bit_length() - 1
     lib = _lib.load()
     dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
     if dev is None:
-        _lib.check(lib.cg_psumbook_build(None, None, 1, 1, 1, 1, 1, None, None))
-    bk_t = torch.from_numpy(np.concatenate([e.astype(np.float16).reshape(-1) for e in ents])).to(dev)
-    x_t = torch.from_numpy(x16.copy()).to(dev)
-    out = torch.empty((len(ents), x16.size // v, k, 1), dtype=torch.float32, device=dev)
+        _lib.check(lib.cg_psumbook_build_f32(None, None, 1, 1, 1, 1, 1, None, None))
+    bk_t = torch.from_numpy(np.concatenate([e.reshape(-1) for e in ents])).to(dev)
+    x_t = torch.from_numpy(x32.copy()).to(dev)
+    out = torch.empty((len(ents), x32.size // v, k, 1), dtype=torch.float32, device=dev)
     s = torch.cuda.current_stream(dev)
-    _lib.check(lib.cg_psumbook_build(bk_t.data_ptr(), x_t.data_ptr(), len(ents), b, v,
-                                     x16.size, 1, out.data_ptr(), ctypes.c_void_p(s.cuda_stream)))
+    _lib.check(lib.cg_psumbook_build_f32(bk_t.data_ptr(), x_t.data_ptr(), len(ents), b, v,
+                                         x32.size, 1, out.data_ptr(),
+                                         ctypes.c_void_p(s.cuda_stream)))
     entries = out[..., 0].cpu().numpy()
     if counters is not None:
-        counters.mac_build += len(ents) * k * x16.size
+        counters.mac_build += len(ents) * k * x32.size
     return Psumbook(entries)

@@ -24,6 +24,7 @@ torch = pytest.importorskip("torch")
 import paper_2512_17970_b200 as cg  # noqa: E402
 from paper_2512_17970_b200 import _lib  # noqa: E402
 from paper_2512_17970_b200 import dist as cgd  # noqa: E402
+from oracle import c_oracle  # noqa: E402
 from oracle import codegemm_oracle as orc  # noqa: E402
 from helpers import assert_within_tolerance  # noqa: E402
 
@@ -48,6 +49,18 @@ def _x0():
     return torch.from_numpy(orc.bench_input_array(2048, 1, 21)).cuda()
 
 
+def _oracle_check(qs, x0, got, what=""):
+    """Each gathered output against the C oracle (the pinned restatement of
+    codegemm_gemm) fed the binary16 rounding of the previous gathered output --
+    the reference's fp16 boundary (cli.py:136) -- within the fast-mode tolerance."""
+    x = x0.cpu().numpy() if hasattr(x0, "cpu") else np.asarray(x0)
+    for i, q in enumerate(qs):
+        ref = c_oracle.codegemm([p.codes for p in q.planes], [b.entries for b in q.books],
+                                q.scales.scales, x.astype(np.float16), 4, 128, threads=8)
+        assert_within_tolerance(got[i], ref, f"{what} layer {i} vs oracle")
+        x = np.asarray(got[i], dtype=np.float32)
+
+
 def _single_gpu_chain(qs, x0, flags):
     layers = [cg.DeviceLayer(q, u=2, flags=flags) for q in qs]
     ys = [torch.empty((r, 1), dtype=torch.float32, device="cuda") for r, _ in SHAPES]
@@ -70,6 +83,7 @@ def test_exchange_world1_chain_matches_staged_chain(det):
             y.fill_(float("nan"))
         cg.gemm_stages(layers, xs, ys, [0, 1, 2], xchg=[PUSH] * 3, comm=comm)
         got = [lay.gathered(comm, i).cpu().numpy() for i in range(3)]
+        _oracle_check(qs, x0, got, "world 1")
         for i in range(3):
             if det:
                 assert np.array_equal(u32(got[i]), u32(ref[i])), i
@@ -100,9 +114,10 @@ def test_exchange_two_ranks_one_stage_per_launch():
                                xchg=[PUSH | (WAIT if i else 0)], comm=comms[r])
         torch.cuda.synchronize()
         for r in range(world):
+            got = [lay.gathered(comms[r], i).cpu().numpy() for i in range(3)]
+            _oracle_check(qs, x0, got, f"rank {r}")
             for i in range(3):
-                got = lay.gathered(comms[r], i).cpu().numpy()
-                assert np.array_equal(u32(got), u32(ref[i])), (rep, r, i)
+                assert np.array_equal(u32(got[i]), u32(ref[i])), (rep, r, i)
 
 
 _CONCURRENT = r"""
@@ -133,9 +148,11 @@ for rep in range(5):
                        stream=streams[r])
     torch.cuda.synchronize()
     for r in range(world):
+        got = [lay.gathered(comms[r], i).cpu().numpy() for i in range(3)]
+        if rep == 0:
+            t._oracle_check(qs, x0, got, f"world {world} rank {r}")
         for i in range(3):
-            got = lay.gathered(comms[r], i).cpu().numpy()
-            assert np.array_equal(t.u32(got), t.u32(ref[i])), (rep, r, i)
+            assert np.array_equal(t.u32(got[i]), t.u32(ref[i])), (rep, r, i)
 print("OK")
 """
 
@@ -198,9 +215,11 @@ for rep in range(3):
                        xchg=[t.PUSH | (t.WAIT if i else 0)], comm=comm)
     torch.cuda.synchronize()
     dist.barrier()
+    got = [lay.gathered(comm, i).cpu().numpy() for i in range(3)]
+    if rep == 0:
+        t._oracle_check(qs, x0, got, f"process rank {rank}")
     for i in range(3):
-        got = lay.gathered(comm, i).cpu().numpy()
-        assert np.array_equal(t.u32(got), t.u32(ref[i])), (rep, rank, i)
+        assert np.array_equal(t.u32(got[i]), t.u32(ref[i])), (rep, rank, i)
     dist.barrier()
 comm.close()
 dist.destroy_process_group()
