@@ -68,6 +68,9 @@ extern "C" {
 /* option flags for cg_layer_options.flags */
 #define CG_OPT_NO_PDL 1        /* launch without programmatic dependent launch        */
 #define CG_OPT_NO_L2_PREFETCH 2 /* skip the bulk L2 prefetch of the CTA's code tiles   */
+#define CG_OPT_BATCH_EAGER 8  /* build the batch (n >= 2) code stream at creation, not on the
+                                 first call with n >= 2                                  */
+#define CG_OPT_NO_BATCH 16    /* n >= 2 runs the per-column Psumbook lookups (comparison)  */
 #define CG_OPT_DETERMINISTIC 4  /* split-K partials summed in a fixed order (run-to-run
                                    bit-identical); default adds them in L2 (faster,
                                    last-bit differences between runs)                  */
@@ -105,6 +108,9 @@ typedef struct cg_layer_info {
     int64_t device_bytes;   /* device memory owned by the handle                       */
     int64_t algorithmic_bytes; /* codes (b bits) + scales + codebooks for one call,
                                    excluding x and y                    */
+    int batch_supported;    /* 1 if n >= 2 calls run the batch kernel (K4: codebook
+                               dequantised into mma.sync fragments, cg_batch.cu)       */
+    int batch_ready;        /* 1 once the batch code stream exists (first n >= 2 call) */
 } cg_layer_info;
 
 int cg_abi_version(void);
@@ -141,6 +147,10 @@ int cg_layer_query(const cg_layer* layer, cg_layer_info* info);
  * y = W x on device buffers, stream-ordered, asynchronous.
  *   x : (cols, n) binary16, row-major (Matrix layout: one column per token)
  *   y : (rows, n) float32, row-major
+ * n == 1 runs the fused Psumbook kernel; n >= 2 (CG_MODE_FAST / AUTO) the batch
+ * kernel when batch_supported (its code stream is built on the first such call,
+ * which then allocates and synchronises), else one Psumbook per column.  Both
+ * batch outputs are deterministic (split-K partials summed in slice order).
  */
 int cg_layer_gemm(cg_layer* layer, const void* x, int n, float* y, int mode, void* stream);
 

@@ -30,6 +30,8 @@ CG_MODE_STRICT = 2
 CG_OPT_NO_PDL = 1
 CG_OPT_NO_L2_PREFETCH = 2
 CG_OPT_DETERMINISTIC = 4
+CG_OPT_BATCH_EAGER = 8
+CG_OPT_NO_BATCH = 16
 
 MODES = {"auto": CG_MODE_AUTO, "fast": CG_MODE_FAST, "strict": CG_MODE_STRICT}
 
@@ -89,6 +91,8 @@ class LayerInfo(ctypes.Structure):
         ("launches_fast", ctypes.c_int),
         ("device_bytes", ctypes.c_int64),
         ("algorithmic_bytes", ctypes.c_int64),
+        ("batch_supported", ctypes.c_int),
+        ("batch_ready", ctypes.c_int),
     ]
 
     def as_dict(self) -> dict:

@@ -17,6 +17,7 @@
 #include <string>
 
 #include "../../include/codegemm_b200.h"
+#include "cg_batch.h"
 #include "cg_internal.h"
 
 namespace {
@@ -201,6 +202,13 @@ struct cg_layer {
     int rg_cap = 0;          // largest rows-per-task whose task buffers fit shared memory (n=1)
     unsigned long long* stamps = nullptr;  // diagnostics (CG_STAMPS=1)
     int64_t device_bytes = 0;
+    // batch path (K4, n >= 2): its code stream, built on first use, and the
+    // split-K partial planes
+    bool batch_ok = false;          // config has a batch kernel
+    uint8_t* bcodes = nullptr;
+    uint16_t* bscl = nullptr;
+    float* bws = nullptr;
+    int64_t bws_bytes = 0;
 };
 
 // One rank's row-shard exchange region (cg_comm_*): a header of counters and
@@ -242,6 +250,9 @@ void free_layer(cg_layer* L) {
     cudaFree(L->grid_flags);
     cudaFree(L->rg_cnt);
     cudaFree(L->stamps);
+    cudaFree(L->bcodes);
+    cudaFree(L->bscl);
+    cudaFree(L->bws);
     cudaFree(L->x_dev);
     cudaFree(L->y_dev);
     cudaFreeHost(L->x_pin);
@@ -617,10 +628,178 @@ int launch_group(cg_layer* const* layers, const uint16_t* const* xs, float* cons
     return CG_OK;
 }
 
+// ---- batch path (K4) ----
+unsigned long long* g_batch_stamps = nullptr;  // diagnostics (CG_STAMPS=1)
+
+// The config has a batch kernel: v in {4, 8}, m in {1, 2}, b <= 8, and scale
+// groups that close at k16-step granularity without straddling a 128-element
+// chunk: g in {16, 32, 64} or a multiple of 128, or one group per row.
+bool batch_config_ok(const cg::Plan& p) {
+    if (!cg::batch_supported_vm(p.v, p.m) || p.b > 8) return false;
+    if (p.g_row || p.g_eff >= p.cols) return true;
+    return p.g_eff == 16 || p.g_eff == 32 || p.g_eff == 64 || p.g_eff % 128 == 0;
+}
+
+// Task geometry of one layer at batch width n: 32 rows x a K-slice; the slice
+// is the whole K when its x^T fits (<= 4096/NT elements), and never straddles
+// a scale group.
+bool plan_batch(const cg::Plan& p, int n, cg::BatchLayer* out, int* smem_out) {
+    if (!batch_config_ok(p)) return false;
+    const int nt = cg::batch_nt_for(n);
+    const int n_rt = (int)((p.rows + 15) / 16);
+    const int n_chunks = (int)((p.cols + 127) / 128);
+    const int rsets = (n_rt + 1) / 2;
+    const bool one_group = p.g_row || p.g_eff >= p.cols;
+    int ks = std::min(n_chunks, 32 / nt);
+    for (; ks >= 1; --ks) {
+        const int64_t kslice = (int64_t)ks * 128;
+        if (!one_group && ks < n_chunks && p.g_eff > kslice && p.g_eff % kslice != 0) continue;
+        const int gis = one_group ? 1 : (int)std::max<int64_t>(1, kslice / p.g_eff);
+        if (cg::batch_layout(p.v, p.m, p.kcount, nt, ks, gis, nullptr) <= 225 * 1024) break;  // (+ the static layer table)
+    }
+    if (ks < 1) return false;
+    cg::BatchLayer b{};
+    b.rows = p.rows;
+    b.cols = p.cols;
+    b.groups = one_group ? 1 : p.groups;
+    b.g_eff = one_group ? ((int64_t)1 << 62) : p.g_eff;
+    b.g_row = one_group ? 1 : 0;
+    b.kcount = p.kcount;
+    b.n_rt = n_rt;
+    b.n_chunks = n_chunks;
+    b.ks_chunks = ks;
+    b.n_slices = (n_chunks + ks - 1) / ks;
+    b.n_rsets = rsets;
+    b.n_tasks = rsets * b.n_slices;
+    const int64_t kslice = (int64_t)ks * 128;
+    if (one_group || p.g_eff >= kslice) {
+        b.spg = ks * 8;  // the whole slice lies in one scale group
+        b.gis = 1;
+    } else {
+        b.spg = (int)(p.g_eff / 16);
+        b.gis = (int)(kslice / p.g_eff);
+    }
+    *out = b;
+    *smem_out = cg::batch_layout(p.v, p.m, p.kcount, nt, ks, b.gis, nullptr);
+    return true;
+}
+
+// the batch code stream and scale tiles, from the uint16 planes recovered on the device
+int ensure_batch_codes(cg_layer* L, cudaStream_t s) {
+    if (L->bcodes) return CG_OK;
+    const cg::Plan& p = L->plan;
+    const bool one_group = p.g_row || p.g_eff >= p.cols;
+    const int64_t bytes = cg::batch_code_bytes(p.rows, p.cols, p.v, p.m);
+    const int64_t groups = one_group ? 1 : p.groups;
+    int rc = dev_alloc(L, &L->bcodes, (size_t)bytes, "batch code stream alloc");
+    if (rc) return rc;
+    rc = dev_alloc(L, &L->bscl, (size_t)cg::batch_scale_bytes(p.rows, groups), "batch scales alloc");
+    if (rc) return rc;
+    uint16_t* raw = L->raw16;
+    bool tmp = false;
+    if (!raw) {
+        CG_CUDA(cudaMalloc(&raw, (size_t)p.m * p.rows * p.segs * 2), "batch prepack staging");
+        tmp = true;
+        cudaError_t e = cg::launch_unpack_codes(p, L->codes, nullptr, raw, s);
+        if (e != cudaSuccess) {
+            cudaFree(raw);
+            return cuda_fail(e, "batch prepack (unpack)");
+        }
+    }
+    // one scale per row: the (rows, 1) plane; else the (rows, groups) plane
+    cudaError_t e = cg::launch_prepack_batch(raw, L->bcodes, p.rows, p.segs, p.m, p.v, L->scales,
+                                             groups, L->bscl, s);
+    if (e == cudaSuccess && tmp) e = cudaStreamSynchronize(s);
+    if (tmp) cudaFree(raw);
+    if (e != cudaSuccess) return cuda_fail(e, "batch prepack");
+    return CG_OK;
+}
+
+int ensure_batch_ws(cg_layer* L, int64_t bytes) {
+    if (bytes <= L->bws_bytes) return CG_OK;
+    cudaFree(L->bws);
+    L->device_bytes -= L->bws_bytes;
+    L->bws = nullptr;
+    L->bws_bytes = 0;
+    int rc = dev_alloc(L, &L->bws, (size_t)bytes, "batch workspace alloc");
+    if (rc) return rc;
+    L->bws_bytes = bytes;
+    return CG_OK;
+}
+
+// One persistent launch of K4 (+ the ordered split-K sum) for `count` layers
+// sharing v and m, over columns [c0, c0 + nb) of x / y (row stride ld).
+int launch_batch(cg_layer* const* layers, const uint16_t* const* xs, float* const* ys, int count,
+                 int ld, int c0, int nb, cudaStream_t s) {
+    cg::BatchParams bp{};
+    bp.n_layers = count;
+    bp.n = nb;
+    bp.ld = ld;
+    const cg::Plan& p0 = layers[0]->plan;
+    const int nt = cg::batch_nt_for(nb);
+    int kc_max = 0, ks_max = 0, gis_max = 0, tasks = 0;
+    for (int i = 0; i < count; ++i) {
+        cg_layer* L = layers[i];
+        int sm = 0;
+        if (!plan_batch(L->plan, nb, &bp.layer[i], &sm))
+            return fail(CG_ERR_UNSUPPORTED, "layer %d has no batch kernel", i);
+        if (reinterpret_cast<uintptr_t>(xs[i]) & 15)
+            return fail(CG_ERR_ARG, "x of layer %d is not 16-byte aligned", i);
+        int rc = ensure_batch_codes(L, s);
+        if (rc) return rc;
+        cg::BatchLayer& b = bp.layer[i];
+        if (b.n_slices > 1) {
+            rc = ensure_batch_ws(L, (int64_t)b.n_slices * L->plan.rows * nb * 4);
+            if (rc) return rc;
+        }
+        b.codes = L->bcodes;
+        b.scl = L->bscl;
+        b.books = L->books;
+        b.x = xs[i] + c0;
+        b.y = ys[i] + c0;
+        b.ws = L->bws;
+        b.x0 = xs[i];
+        kc_max = std::max(kc_max, b.kcount);
+        ks_max = std::max(ks_max, b.ks_chunks);
+        gis_max = std::max(gis_max, b.gis);
+        tasks += b.n_tasks;
+    }
+    bp.total_tasks = tasks;
+    if (std::getenv("CG_STAMPS")) {  // diagnostics: one stamp buffer per process
+        if (!g_batch_stamps && cudaMalloc(&g_batch_stamps, 64 * 1024 * 8) == cudaSuccess)
+            cudaMemset(g_batch_stamps, 0, 64 * 1024 * 8);
+        bp.stamps = g_batch_stamps;
+    }
+    const int smem = cg::batch_layout(p0.v, p0.m, kc_max, nt, ks_max, gis_max, &bp);
+    if (smem > 225 * 1024)
+        return fail(CG_ERR_CONFIG, "batch launch does not fit in shared memory (%d bytes)", smem);
+    // every layer's code tiles must fit the buffer stride of the largest slice
+    const int grid = std::min(tasks, layers[0]->sms);
+    CG_CUDA(cg::launch_batch_gemm(p0.v, p0.m, nt, bp, grid, smem, s,
+                                  !(layers[0]->flags & CG_OPT_NO_PDL)),
+            "batch gemm launch");
+    return CG_OK;
+}
+
+// n >= 2 through K4 in column blocks of <= 32
+int run_batch(cg_layer* const* layers, const uint16_t* const* xs, float* const* ys, int count,
+              int n, cudaStream_t s) {
+    for (int c0 = 0; c0 < n; c0 += 32) {
+        const int nb = std::min(32, n - c0);
+        int rc = launch_batch(layers, xs, ys, count, n, c0, nb, s);
+        if (rc) return rc;
+    }
+    return CG_OK;
+}
+
+bool use_batch(const cg_layer* L, int n) {
+    return n >= 2 && L->batch_ok && !(L->flags & CG_OPT_NO_BATCH);
+}
+
 int run_gemm(cg_layer* L, const uint16_t* x, int n, float* y, int mode, cudaStream_t s) {
     const cg::Plan& p = L->plan;
-    if (mode == CG_MODE_AUTO) mode = p.fast ? CG_MODE_FAST : CG_MODE_STRICT;
-    if (mode == CG_MODE_FAST && !p.fast)
+    if (mode == CG_MODE_AUTO) mode = (p.fast || use_batch(L, n)) ? CG_MODE_FAST : CG_MODE_STRICT;
+    if (mode == CG_MODE_FAST && !p.fast && !use_batch(L, n))
         return fail(CG_ERR_UNSUPPORTED,
                     "no fused kernel for v=%d m=%d b=%d g=%lld at cols=%lld; use CG_MODE_STRICT",
                     p.v, p.m, p.b, (long long)p.g, (long long)p.cols);
@@ -633,6 +812,7 @@ int run_gemm(cg_layer* L, const uint16_t* x, int n, float* y, int mode, cudaStre
     cg_layer* one[1] = {L};
     const uint16_t* xs[1] = {x};
     float* ys[1] = {y};
+    if (use_batch(L, n)) return run_batch(one, xs, ys, 1, n, s);
     return launch_group(one, xs, ys, 1, n, s);
 }
 
@@ -812,6 +992,11 @@ int create_layer(const uint16_t* const* codes, const uint8_t* const* packed,
         if ((rc = dev_alloc(L, &L->grid_flags, fb, "grid barrier flags"))) return bail(rc);
         cudaMemset(L->grid_flags, 0, fb);
     }
+    L->batch_ok = batch_config_ok(p) && (p.fast || L->raw16);
+    if (L->batch_ok && (L->flags & CG_OPT_BATCH_EAGER)) {
+        if ((rc = ensure_batch_codes(L, s))) return bail(rc);
+        if (cudaStreamSynchronize(s) != cudaSuccess) return bail(fail(CG_ERR_CUDA, "batch prepack"));
+    }
     if (p.fast && std::getenv("CG_STAMPS")) {
         if ((rc = dev_alloc(L, &L->stamps, (size_t)L->sms * 1024, "stamps"))) return bail(rc);
         cudaMemset(L->stamps, 0, (size_t)L->sms * 1024);
@@ -864,6 +1049,8 @@ int cg_layer_query(const cg_layer* L, cg_layer_info* info) {
     // codes at b bits + binary16 scales + binary16 codebooks
     info->algorithmic_bytes = (p.rows * p.segs * p.m * p.b + 7) / 8 + 2 * p.rows * p.groups +
                               2LL * p.m * p.kcount * p.v;
+    info->batch_supported = L->batch_ok && !(L->flags & CG_OPT_NO_BATCH) ? 1 : 0;
+    info->batch_ready = L->bcodes ? 1 : 0;
     return CG_OK;
 }
 
@@ -884,6 +1071,13 @@ int cg_gemm_group(cg_layer* const* layers, const void* const* xs, float* const* 
     for (int i = 0; i < count; ++i)
         if (!layers[i] || !xs[i] || !ys[i]) return fail(CG_ERR_ARG, "NULL entry %d", i);
     DeviceGuard guard(layers[0]->device);
+    bool batch = count <= cg::kMaxBatchGroup;
+    for (int i = 0; i < count && batch; ++i)
+        batch = use_batch(layers[i], n) && layers[i]->plan.v == layers[0]->plan.v &&
+                layers[i]->plan.m == layers[0]->plan.m;
+    if (batch)
+        return run_batch(layers, reinterpret_cast<const uint16_t* const*>(xs), ys, count, n,
+                         static_cast<cudaStream_t>(stream));
     return launch_group(layers, reinterpret_cast<const uint16_t* const*>(xs), ys, count, n,
                         static_cast<cudaStream_t>(stream));
 }
@@ -1202,6 +1396,15 @@ int cg_psumbook_build_f32(const float* books, const float* x, int m, int b, int 
 }
 
 }  // extern "C"
+
+// Diagnostics only: the batch kernel's stamps of the last launch (CG_STAMPS=1)
+extern "C" int cg_debug_batch_stamps(unsigned long long* host, int64_t count) {
+    if (!g_batch_stamps) return fail(CG_ERR_ARG, "no batch stamps (set CG_STAMPS=1)");
+    CG_CUDA(cudaMemcpy(host, g_batch_stamps, std::min<int64_t>(count, 64 * 1024) * 8,
+                       cudaMemcpyDeviceToHost),
+            "stamps D2H");
+    return CG_OK;
+}
 
 // Diagnostics only (not part of the ABI header): copy the per-CTA phase
 // timestamps of the last fused launch (CG_STAMPS=1 at layer creation).

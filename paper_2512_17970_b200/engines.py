@@ -210,6 +210,13 @@ class DeviceLayer:
     def handle(self):
         return self._handle
 
+    def query(self) -> dict:
+        """Re-read the handle's info (batch_ready changes on the first n >= 2 call)."""
+        info = _lib.LayerInfo()
+        _lib.check(self._lib.cg_layer_query(self._handle, ctypes.byref(info)))
+        self.info = info.as_dict()
+        return self.info
+
     # -- host buffers -------------------------------------------------------
     def gemm_host(self, x_f16: np.ndarray, mode: str = "auto") -> np.ndarray:
         x = np.ascontiguousarray(x_f16, dtype=np.float16)
