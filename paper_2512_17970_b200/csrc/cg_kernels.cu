@@ -355,22 +355,14 @@ __device__ __forceinline__ void load_centroid(float (&c)[V], const uint16_t* p) 
     }
 }
 
-// entries of codes c (4 lanes 4q..4q+3) for one sub-table: 2 FFMA2 chains
-template <int V>
-__device__ __forceinline__ void psum_entries(float* dst, const float (&cc)[V],
-                                             const float2 (&x01)[V], const float2 (&x23)[V]) {
-    float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-        a01 = __ffma2_rn(make_float2(cc[k], cc[k]), x01[k], a01);
-        a23 = __ffma2_rn(make_float2(cc[k], cc[k]), x23[k], a23);
-    }
-    *reinterpret_cast<float4*>(dst) = make_float4(a01.x, a01.y, a23.x, a23.y);
-}
-
-// books16: raw binary16 codebooks [t][kcount][V];  xs: staged x pairs
-template <int V, int M, int U, int KB>
-__device__ __forceinline__ void build_psumbook_smem(float* psum, const uint16_t* books16,
+// books16: raw binary16 codebooks [t][kcount][V];  xs: staged x pairs.
+// FULL (kcount == 2**KB, every b = 8 / b = 4 table): no per-code bounds test,
+// so the kCPT codes' 2*kCPT FFMA2 chains of a sub-table are interleaved
+// k-outer (independent chains back to back; a per-code branch would serialise
+// them and expose the FFMA2 latency).  Each entry is still the chain
+// ((+0 + c0*x0) + c1*x1) + ... of exact products: bit-exact.
+template <int V, int M, int U, int KB, bool FULL>
+__device__ __forceinline__ void build_psumbook_impl(float* psum, const uint16_t* books16,
                                                     const float* xs, int kcount, int tid) {
     using S = FusedShape<V, M, U, KB>;
     const int lane = tid & 31, warp = tid >> 5;
@@ -378,7 +370,6 @@ __device__ __forceinline__ void build_psumbook_smem(float* psum, const uint16_t*
     const int csub = lane >> 3;  // 4 codes per warp per pass
     const int c0 = csub + 4 * warp;
     constexpr int kCPT = S::kCPT;
-    const bool full = S::kFullCodes && kcount == S::kCodes;
 #pragma unroll 1
     for (int t = 0; t < M; ++t) {
         const uint16_t* bk = books16 + t * kcount * V;
@@ -387,7 +378,11 @@ __device__ __forceinline__ void build_psumbook_smem(float* psum, const uint16_t*
 #pragma unroll
             for (int i = 0; i < kCPT; ++i) {
                 const int c = c0 + 4 * kWarps * i;
-                if (full || c < kcount) load_centroid<V>(cc[i], bk + c * V);
+                if (FULL || c < kcount) load_centroid<V>(cc[i], bk + c * V);
+                else {
+#pragma unroll
+                    for (int k = 0; k < V; ++k) cc[i][k] = 0.0f;
+                }
             }
         }
 #pragma unroll 1
@@ -408,21 +403,50 @@ __device__ __forceinline__ void build_psumbook_smem(float* psum, const uint16_t*
             }
             float* dst = psum + (j >> 1) * S::kRegionFloats + (j & 1) * 32 + q * 4;
             if constexpr (S::kHoist) {
+                float2 a01[kCPT], a23[kCPT];
+#pragma unroll
+                for (int k = 0; k < V; ++k)
+#pragma unroll
+                    for (int i = 0; i < kCPT; ++i) {
+                        const float2 cb = make_float2(cc[i][k], cc[i][k]);
+                        a01[i] = k == 0 ? __ffma2_rn(cb, x01[0], make_float2(0.0f, 0.0f))
+                                        : __ffma2_rn(cb, x01[k], a01[i]);
+                        a23[i] = k == 0 ? __ffma2_rn(cb, x23[0], make_float2(0.0f, 0.0f))
+                                        : __ffma2_rn(cb, x23[k], a23[i]);
+                    }
 #pragma unroll
                 for (int i = 0; i < kCPT; ++i) {
                     const int c = c0 + 4 * kWarps * i;
-                    if (full || c < kcount) psum_entries<V>(dst + c * 64, cc[i], x01, x23);
+                    if (FULL || c < kcount)
+                        *reinterpret_cast<float4*>(dst + c * 64) =
+                            make_float4(a01[i].x, a01[i].y, a23[i].x, a23[i].y);
                 }
             } else {
 #pragma unroll 1
                 for (int c = c0; c < kcount; c += 4 * kWarps) {
                     float ci[V];
                     load_centroid<V>(ci, bk + c * V);
-                    psum_entries<V>(dst + c * 64, ci, x01, x23);
+                    float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
+#pragma unroll
+                    for (int k = 0; k < V; ++k) {
+                        a01 = __ffma2_rn(make_float2(ci[k], ci[k]), x01[k], a01);
+                        a23 = __ffma2_rn(make_float2(ci[k], ci[k]), x23[k], a23);
+                    }
+                    *reinterpret_cast<float4*>(dst + c * 64) = make_float4(a01.x, a01.y, a23.x, a23.y);
                 }
             }
         }
     }
+}
+
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void build_psumbook_smem(float* psum, const uint16_t* books16,
+                                                    const float* xs, int kcount, int tid) {
+    using S = FusedShape<V, M, U, KB>;
+    if (S::kFullCodes && kcount == S::kCodes)
+        build_psumbook_impl<V, M, U, KB, true>(psum, books16, xs, kcount, tid);
+    else
+        build_psumbook_impl<V, M, U, KB, false>(psum, books16, xs, kcount, tid);
 }
 
 // ---------------------------------------------------------------------------

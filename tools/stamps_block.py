@@ -97,8 +97,7 @@ for k in range(11):
             show(f"task{k} {nm}", st[:, k * 8 + slot])
 for b in range(7):
     for j, nm in enumerate(("entered", "drained", "arrived", "released")):
-        if j in (0, 3):
-            show(f"barrier{b} {nm}", st[:, 96 + 4 * b + j])
+        show(f"barrier{b} {nm}", st[:, 96 + 4 * b + j])
 for b in range(4):
     show(f"xchg{b} pushed", st[:, 112 + 2 * b])
     show(f"xchg{b} all arrived", st[:, 113 + 2 * b])
