@@ -86,6 +86,14 @@ def make_layer(rows, cols, cfg, seed):
     return cg.random_layer(rows, cols, qc, seed=seed)
 
 
+def bench_config(args, n: int, world: int) -> dict:
+    """The workload dict both arms print (identical, so the driver's same_config holds)."""
+    return {"workload": f"llama{args.workload} decoder-block linears (reference suite x "
+                        f"multiplicity), {args.config}, batch {n}",
+            "config": args.config, "batch": n, "layers_per_step": len(block_spec(args.workload)),
+            "parallelism": (f"rows sharded over {world} GPUs" if world > 1 else "single GPU")}
+
+
 def layer_seed(copy: int, idx: int, rows: int, cols: int) -> int:
     # copy 0, first layer of each shape: the reference's bench_layer seed (bench.py:168-170)
     return (0 ^ rows ^ cols) if copy == 0 and idx == 0 else 1_000_003 * (copy + 1) + 7919 * idx
@@ -232,14 +240,146 @@ def run_reference(args, spec, cfg, n, rank, world):
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u8/f16->f32",
         "data": "synthetic (reference generators: random_layer, bench_input)",
-        "config": {"workload": f"llama{args.workload} decoder-block linears, {args.config}, "
-                               f"batch {n}", "config": args.config, "batch": n},
+        "config": bench_config(args, n, world),
+        "setup": "CPU: the numpy restatement of the reference engine (oracle/codegemm_oracle.py), "
+                 "same layers and inputs as the GPU arm",
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "port",
                          "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- extras
+GQA_8B = (("qkv (fused q,k,v GQA)", 6144, 4096), ("o", 4096, 4096), ("gate", 14336, 4096),
+          ("up", 14336, 4096), ("down", 4096, 14336))
+GQA_STAGES = (0, 1, 2, 2, 3)
+GQA_XSRC = (None, 0, 1, 1, 2)
+
+
+def measure_extras(args, cfg, n, blocks, spec, kern, ref_api_layers, peak, capture, timed, stream,
+                   dev):
+    """Secondary lines of the N=1 run (SURVEY.md §8d configs 1, 2-GQA, 4 and the
+    reference-API end-to-end leg).  Each is device time over CUDA graphs with
+    weights rotated over copies larger than L2, except the e2e leg (wall clock)."""
+    import torch
+
+    import paper_2512_17970_b200 as cg
+    from oracle import codegemm_oracle as orc
+
+    out = {}
+    # ---- config 1: one 4096x4096 layer alone (back-to-back launches, rotating copies)
+    if "attn_proj" in kern:
+        us = kern["attn_proj"][0]
+        b1 = layer_bytes(4096, 4096, cfg, n)
+        out["config1_layer"] = {"shape": "4096x4096", "us_per_launch": round(us, 3),
+                                "GB/s": round(b1 / (us * 1e-6) / 1e9, 1),
+                                "frac_of_measured_hbm": round(b1 / (us * 1e-6) / 1e9 / peak, 4),
+                                "bytes": b1,
+                                "note": "one fused launch per layer: its fixed cost (launch, "
+                                        "Psumbook build, split-K flush) is not amortised over a "
+                                        "block"}
+    # ---- config 2 with the real Llama-3-8B GQA shapes (fused qkv 6144x4096)
+    try:
+        gq_bytes = sum(layer_bytes(r, c, cfg, n) for _, r, c in GQA_8B)
+        gw = sum(layer_bytes(r, c, cfg, n, with_io=False) for _, r, c in GQA_8B)
+        gcopies = max(2, -(-3 * L2_BYTES // gw))
+        gblocks = []
+        for cp in range(gcopies):
+            lay = [cg.DeviceLayer(make_layer(r, c, cfg, 77_000 + 100 * cp + i), u=TILING_U)
+                   for i, (_, r, c) in enumerate(GQA_8B)]
+            x0 = torch.from_numpy(orc.bench_input_array(4096, n, 500 + cp)).to(dev)
+            ys = [torch.empty((r, n), dtype=torch.float32, device=dev) for _, r, c in GQA_8B]
+            # o reads the q rows of the fused qkv output (the attention output's width)
+            xs = [x0 if src is None else (ys[src][:4096] if src == 0 else ys[src])
+                  for src in GQA_XSRC]
+            gblocks.append(cg.StagedLaunch(lay, xs, ys, list(GQA_STAGES)))
+        g = capture(lambda: [b() for b in gblocks])
+        timed([g], 3 * gcopies, gcopies)
+        reps = 50 * gcopies
+        us = timed([g], reps, gcopies) / reps * 1e3
+        out["gqa_block"] = {"shapes": [f"{nm} {r}x{c}" for nm, r, c in GQA_8B],
+                            "us_per_block": round(us, 3),
+                            "GB/s": round(gq_bytes / (us * 1e-6) / 1e9, 1),
+                            "frac_of_measured_hbm": round(gq_bytes / (us * 1e-6) / 1e9 / peak, 4),
+                            "bytes_per_block": gq_bytes,
+                            "launch": "one staged launch per block: {qkv} -> {o} -> {gate,up} "
+                                      "-> {down}, real data dependencies; "
+                                      f"{gcopies} block copies rotated"}
+        del gblocks, g
+    except Exception as e:  # (a secondary line never sinks the bench)
+        out["gqa_block"] = {"error": repr(e)[:200]}
+    # ---- config 4: batch sweep on the 8B block (reference protocol: layers timed
+    #      independently, block = sum over the suite with multiplicities); the same
+    #      shapes as dense binary16 weights through cuBLAS for comparison
+    try:
+        sweep = []
+        uniq = {}
+        for idx, (name, r, c) in enumerate(spec):
+            uniq.setdefault(name, (idx, r, c, 0))
+            uniq[name] = (uniq[name][0], r, c, uniq[name][3] + 1)
+        # (dense: 4 distinct weight copies per shape, > L2 together for every shape)
+        dense_w = {name: [torch.randn((r, c), device=dev, dtype=torch.float16) * 0.02
+                          for _ in range(4)] for name, (idx, r, c, mult) in uniq.items()}
+        for nb in (4, 8, 16, 32):
+            per, per_dense = {}, {}
+            for name, (idx, r, c, mult) in uniq.items():
+                xs = [torch.from_numpy(orc.bench_input_array(c, nb, k)).to(dev)
+                      for k in range(len(blocks))]
+                ys = [torch.empty((r, nb), dtype=torch.float32, device=dev)
+                      for _ in range(len(blocks))]
+                lays = [blocks[k][idx]["layer"] for k in range(len(blocks))]
+                gk = capture(lambda lays=lays, xs=xs, ys=ys: [l.gemm(x, y) for l, x, y in
+                                                               zip(lays, xs, ys)])
+                timed([gk], 2)
+                rr = 20
+                per[name] = timed([gk], rr) / (rr * len(blocks)) * 1e3
+                xd = xs[0]
+                gd = capture(lambda ws=dense_w[name], xd=xd: [torch.matmul(w, xd) for w in ws])
+                timed([gd], 2)
+                per_dense[name] = timed([gd], rr) / (rr * 4) * 1e3
+                del gk, gd
+            blk = sum(per[nm] * m for nm, (i, r, c, m) in uniq.items())
+            blk_d = sum(per_dense[nm] * m for nm, (i, r, c, m) in uniq.items())
+            byt = sum(layer_bytes(r, c, cfg, nb) * m for nm, (i, r, c, m) in uniq.items())
+            sweep.append({"batch": nb, "kernel": "K4 batch (mma.sync, codebook dequantised "
+                                                 "in registers)",
+                          "us_per_layer": {f"{nm} {r}x{c}": round(per[nm], 2)
+                                           for nm, (i, r, c, m) in uniq.items()},
+                          "us_per_block": round(blk, 2),
+                          "GB/s": round(byt / (blk * 1e-6) / 1e9, 1),
+                          "cublas_fp16_dense_us_per_block": round(blk_d, 2),
+                          "dense_note": "torch.matmul of binary16 weights (4 copies per shape "
+                                        "rotated), the paper's A.4 comparison"})
+        out["batch_sweep"] = sweep
+        del dense_w
+    except Exception as e:
+        out["batch_sweep"] = {"error": repr(e)[:200]}
+    # ---- end to end the way a reference user calls it: codegemm_gemm(q, Matrix(x))
+    #      per layer with numpy buffers (engines.py:245-263; timed like bench.py:192-214)
+    try:
+        xs_h = [cg.Matrix(orc.bench_input_array(q.cols, n, 900 + i))
+                for i, q in enumerate(ref_api_layers)]
+        for q, x in zip(ref_api_layers, xs_h):  # warm-up: uploads and prepacks once per layer
+            cg.codegemm_gemm(q, x)
+        steps = 20
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            for q, x in zip(ref_api_layers, xs_h):
+                cg.codegemm_gemm(q, x)
+        dt = (time.perf_counter() - t0) / steps
+        byt = sum(layer_bytes(q.rows, q.cols, cfg, n) for q in ref_api_layers)
+        out["e2e_reference_api"] = {
+            "value": round(byt / dt / 1e9, 3), "unit": "GB/s", "ms_per_step": round(dt * 1e3, 3),
+            "h2d_bytes_per_step": sum(2 * q.cols * n for q in ref_api_layers),
+            "d2h_bytes_per_step": sum(4 * q.rows * n for q in ref_api_layers),
+            "path": "per step: the 7 layers of one block, each codegemm_gemm(q, Matrix(x)) -> "
+                    "(numpy y, OpCounters): host x copied in, one deterministic fused launch, "
+                    "y copied out, synchronised; wall clock"}
+    except Exception as e:
+        out["e2e_reference_api"] = {"error": repr(e)[:200]}
+    return out
 
 
 # --------------------------------------------------------------------------- GPU
@@ -254,6 +394,8 @@ def main():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="also time every unique shape alone")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the config-1 / GQA / batch-sweep / reference-API lines")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -309,6 +451,7 @@ def main():
     #      each way.
     in_elems = sum(c * n for i, (_, r, c) in enumerate(spec) if STEP_XSRC[i] is None)
     blocks, xbufs, ybufs = [], [], []
+    ref_api_layers = []  # copy 0's QuantizedLayers: the reference-API end-to-end leg
     for cp in range(copies):
         layers = []
         xbuf = torch.empty(in_elems, dtype=torch.float16, device=dev)
@@ -317,6 +460,8 @@ def main():
         xo = yo = 0
         for idx, (name, rows, cols) in enumerate(spec):
             q = make_layer(rows, cols, cfg, layer_seed(cp, idx, rows, cols))
+            if cp == 0 and world == 1:
+                ref_api_layers.append(q)
             sl = (ShardedLayer(q, rank, world, u=TILING_U) if world > 1
                   else cg.DeviceLayer(q, u=TILING_U))
             x = torch.from_numpy(orc.bench_input_array(cols, n, cp * 31 + idx)).to(dev)
@@ -645,6 +790,11 @@ def main():
                               "inputs, the prepared staged exchange launch, one pinned D2H of all "
                               "7 gathered outputs, sync; wall clock, max over ranks"}
 
+    extras = {}
+    if world == 1 and not args.no_extras:
+        extras = measure_extras(args, cfg, n, blocks, spec, kern, ref_api_layers, peak, capture,
+                                timed, stream, dev)
+
     base = base_c = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         base, base_c = cpu_baseline(spec, cfg, n)
@@ -657,26 +807,24 @@ def main():
             "vs_baseline": None, "dtype": "u8 codes, f16 in, f32 accumulate",
             "data": "synthetic (reference generators random_layer/bench_input; random codebooks, "
                     "codes, scales)",
-            "config": {"workload": f"llama{args.workload} decoder-block linears (reference suite "
-                                   f"x multiplicity), {args.config}, batch {n}",
-                       "config": args.config, "batch": n,
-                       "layers_per_step": len(spec), "weight_copies": copies,
-                       "l2": f"inputs larger than L2: {copies} distinct block copies rotated "
-                             f"({copies * weight_bytes / 2**20:.0f} MiB of weights per rank)",
-                       "parallelism": f"rows sharded over {world} GPUs, all-gathers fused "
-                                      "into the kernel over NVLink peer stores"
-                       if world > 1 else "single GPU",
-                       "launch": ("one persistent staged launch (cg_gemm_stages) per "
-                                  f"{CHAIN} steps: {CHAIN} block copies chained "
-                                  "as a layer stack, each block the stages {q,k,v} -> {o} -> "
-                                  "{gate,up} -> {down}; o/gate/up/down read the previous stage's "
-                                  "y and the next block's q,k,v read y_down, rounded to fp16; "
-                                  f"grid barriers between stages, u={TILING_U}; CUDA graph")
-                       if world == 1 else
-                       "per step: ONE staged exchange launch per rank (cg_gemm_stages_xchg): "
-                       "stages {q,k,v} -> {o} -> {gate,up} -> {down}, every layer's rows "
-                       "pushed to every peer after its stage, the next stage reading the "
-                       "gathered y; CUDA graph per block copy, PDL"},
+            "config": bench_config(args, n, world),
+            "setup": {"weight_copies": copies,
+                      "l2": f"inputs larger than L2: {copies} distinct block copies rotated "
+                            f"({copies * weight_bytes / 2**20:.0f} MiB of weights per rank)",
+                      "parallelism": f"rows sharded over {world} GPUs, all-gathers fused "
+                                     "into the kernel over NVLink peer stores"
+                      if world > 1 else "single GPU",
+                      "launch": ("one persistent staged launch (cg_gemm_stages) per "
+                                 f"{CHAIN} steps: {CHAIN} block copies chained "
+                                 "as a layer stack, each block the stages {q,k,v} -> {o} -> "
+                                 "{gate,up} -> {down}; o/gate/up/down read the previous stage's "
+                                 "y and the next block's q,k,v read y_down, rounded to fp16; "
+                                 f"grid barriers between stages, u={TILING_U}; CUDA graph")
+                      if world == 1 else
+                      "per step: ONE staged exchange launch per rank (cg_gemm_stages_xchg): "
+                      "stages {q,k,v} -> {o} -> {gate,up} -> {down}, every layer's rows "
+                      "pushed to every peer after its stage, the next stage reading the "
+                      "gathered y; CUDA graph per block copy, PDL"},
             "us_per_layer": us_per_layer,
             "us_per_layer_staged_chain": us_chain,
             "us_per_block": round(ms_per_step * 1e3, 3),
@@ -692,6 +840,7 @@ def main():
                                  "launches_per_step": len(groups),
                                  "all_gather": None if world == 1 else "NCCL, one per layer"},
             "roofline": roofline,
+            **extras,
             "cpu_baseline": base, "cpu_baseline_c": base_c,
             "e2e": e2e,
             "gpu_launches": (args.steps // spg * (spg // CHAIN) + args.steps % spg) if world == 1

@@ -169,7 +169,8 @@ void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms, int reserved) {
         }
     }
     if (p.fast) {
-        p.code_bytes = p.n_slices * p.n_rg * (int64_t)p.m * 16 * p.slice_segs;
+        // one byte per code, or two per byte for 16-entry tables (b <= 4)
+        p.code_bytes = p.n_slices * p.n_rg * (int64_t)p.m * 16 * p.slice_segs / (p.kbits == 4 ? 2 : 1);
         p.scale_bytes = p.n_slices * p.n_rg * (int64_t)p.n_gs * 16 * 2;
     }
 }
@@ -640,9 +641,9 @@ bool batch_config_ok(const cg::Plan& p) {
     return p.g_eff == 16 || p.g_eff == 32 || p.g_eff == 64 || p.g_eff % 128 == 0;
 }
 
-// Task geometry of one layer at batch width n: 32 rows x a K-slice; the slice
-// is the whole K when its x^T fits (<= 4096/NT elements), and never straddles
-// a scale group.
+// Task geometry of one layer at batch width n: 32 rows x a K-slice of at most
+// 4096/NT elements (equal slices), shrunk until it fits shared memory and
+// never straddling a scale group.
 bool plan_batch(const cg::Plan& p, int n, cg::BatchLayer* out, int* smem_out) {
     if (!batch_config_ok(p)) return false;
     const int nt = cg::batch_nt_for(n);
@@ -650,7 +651,11 @@ bool plan_batch(const cg::Plan& p, int n, cg::BatchLayer* out, int* smem_out) {
     const int n_chunks = (int)((p.cols + 127) / 128);
     const int rsets = (n_rt + 1) / 2;
     const bool one_group = p.g_row || p.g_eff >= p.cols;
+    // slices of at most 4096/NT elements (measured: one slice of a larger x^T tile
+    // costs more in staging and occupancy than the extra partial plane), all
+    // slices the same width
     int ks = std::min(n_chunks, 32 / nt);
+    ks = (n_chunks + ((n_chunks + ks - 1) / ks) - 1) / ((n_chunks + ks - 1) / ks);
     for (; ks >= 1; --ks) {
         const int64_t kslice = (int64_t)ks * 128;
         if (!one_group && ks < n_chunks && p.g_eff > kslice && p.g_eff % kslice != 0) continue;

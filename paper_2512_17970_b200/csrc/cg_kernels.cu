@@ -79,8 +79,25 @@ __host__ __device__ __forceinline__ int row_mask(int lane) {
     return ((lane & 1) << 3) | ((lane >> 1 & 1) << 2) | ((lane >> 2 & 1) << 1) | (lane >> 3 & 1);
 }
 
-__device__ __forceinline__ int64_t packed_index(int64_t t, int64_t r, int64_t seg, int m, int u,
-                                                int64_t n_rg) {
+// Byte mode (b > 4): one byte per code; the lane's 16*u bytes of a (slice, row
+// group, codebook) tile are [slot][u] code indices idx = slot*u + uu, in u
+// chunks of 16 bytes laid out lane-contiguous: byte idx&15 of chunk idx>>4.
+// Nibble mode (b <= 4, 16-entry tables): two codes per byte, 8*u bytes per
+// lane and tile.  Code idx sits in 32-bit word idx>>3 of the lane, byte idx&3,
+// low nibble if (idx&4) == 0 else high nibble -- so masking a word with
+// 0x0f0f0f0f (or shifting it right by 4 first) yields four codes as bytes and
+// the gather's byte extraction is unchanged.  Words are laid out in 16-byte
+// chunks lane-contiguous (u >= 2) or as 8 bytes per lane (u = 1).
+__host__ __device__ __forceinline__ int64_t tile_bytes_of(int u, bool nib) {
+    return nib ? (int64_t)u * 256 : (int64_t)u * 512;
+}
+// byte offset of the lane's 32-bit word wi (nibble mode) inside a tile
+__host__ __device__ __forceinline__ int64_t nib_word_off(int u, int lane, int wi) {
+    return u >= 2 ? ((int64_t)(wi >> 2) * 32 + lane) * 16 + (wi & 3) * 4 : (int64_t)lane * 8 + wi * 4;
+}
+
+__device__ __forceinline__ uint32_t packed_code(const uint8_t* packed, int64_t t, int64_t r,
+                                                int64_t seg, int m, int u, int64_t n_rg, bool nib) {
     const int64_t slice_segs = 32 * u;
     const int64_t slice = seg / slice_segs;
     const int64_t within = seg - slice * slice_segs;
@@ -89,9 +106,11 @@ __device__ __forceinline__ int64_t packed_index(int64_t t, int64_t r, int64_t se
     const int64_t rg = r >> 4;
     const int64_t rr = r & 15;
     const int64_t slot = rr ^ row_mask((int)lane);
-    const int64_t idx = slot * u + uu;  // position in the lane's [slot][u] bytes
-    const int64_t tile = ((slice * n_rg + rg) * m + t) * (int64_t)(u * 512);
-    return tile + (idx >> 4) * 512 + lane * 16 + (idx & 15);
+    const int64_t idx = slot * u + uu;  // position in the lane's [slot][u] codes
+    const int64_t tile = ((slice * n_rg + rg) * m + t) * tile_bytes_of(u, nib);
+    if (!nib) return packed[tile + (idx >> 4) * 512 + lane * 16 + (idx & 15)];
+    const uint8_t byte = packed[tile + nib_word_off(u, (int)lane, (int)(idx >> 3)) + (idx & 3)];
+    return (idx & 4) ? (byte >> 4) : (byte & 15u);
 }
 
 // ---------------------------------------------------------------------------
@@ -100,11 +119,11 @@ __device__ __forceinline__ int64_t packed_index(int64_t t, int64_t r, int64_t se
 __global__ void prepack_codes_kernel(const uint16_t* __restrict__ raw, uint8_t* __restrict__ out,
                                      int64_t total, int64_t rows, int64_t segs, int m, int u,
                                      int64_t n_rg, uint32_t code_limit,
-                                     unsigned* __restrict__ bad) {
-    // one thread per output byte, decoding (slice, rg, t, chunk, lane, byte)
+                                     unsigned* __restrict__ bad, int nib) {
+    // one thread per output byte, decoding (slice, rg, t, lane, position)
+    const int64_t tile_bytes = tile_bytes_of(u, nib != 0);
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
          o += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t tile_bytes = (int64_t)u * 512;
         int64_t rest = o;
         const int64_t in_tile = rest % tile_bytes;
         rest /= tile_bytes;
@@ -112,19 +131,41 @@ __global__ void prepack_codes_kernel(const uint16_t* __restrict__ raw, uint8_t* 
         rest /= m;
         const int64_t rg = rest % n_rg;
         const int64_t slice = rest / n_rg;
-        const int64_t chunk = in_tile / 512;
-        const int64_t lane = (in_tile % 512) / 16;
-        const int64_t idx = chunk * 16 + (in_tile % 16);
-        const int64_t slot = idx / u, uu = idx % u;
-        const int64_t r = rg * 16 + (slot ^ row_mask((int)lane));
-        const int64_t seg = slice * 32 * u + lane * u + uu;
-        uint8_t val = 0;
-        if (r < rows && seg < segs) {
-            const uint16_t c = raw[(t * rows + r) * segs + seg];
-            if (c >= code_limit) atomicOr(bad, 1u);
-            val = static_cast<uint8_t>(c);
+        int64_t lane, idx[2];
+        int ncodes;
+        if (!nib) {
+            const int64_t chunk = in_tile / 512;
+            lane = (in_tile % 512) / 16;
+            idx[0] = chunk * 16 + (in_tile % 16);
+            ncodes = 1;
+        } else {
+            int64_t wi, bw;
+            if (u >= 2) {
+                const int64_t chunk = in_tile / 512;
+                lane = (in_tile % 512) / 16;
+                wi = chunk * 4 + (in_tile % 16) / 4;
+                bw = in_tile % 4;
+            } else {
+                lane = in_tile / 8;
+                wi = (in_tile % 8) / 4;
+                bw = in_tile % 4;
+            }
+            idx[0] = wi * 8 + bw;  // low nibble
+            idx[1] = idx[0] + 4;   // high nibble
+            ncodes = 2;
         }
-        out[o] = val;
+        uint32_t val = 0;
+        for (int k = 0; k < ncodes; ++k) {
+            const int64_t slot = idx[k] / u, uu = idx[k] % u;
+            const int64_t r = rg * 16 + (slot ^ row_mask((int)lane));
+            const int64_t seg = slice * 32 * u + lane * u + uu;
+            if (r < rows && seg < segs) {
+                const uint16_t c = raw[(t * rows + r) * segs + seg];
+                if (c >= code_limit) atomicOr(bad, 1u);
+                val |= (uint32_t)c << (4 * k);
+            }
+        }
+        out[o] = static_cast<uint8_t>(val);
     }
 }
 
@@ -160,7 +201,8 @@ __global__ void check_codes_kernel(const uint16_t* __restrict__ raw, int64_t tot
 
 __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed,
                                     const uint16_t* __restrict__ raw16, uint16_t* __restrict__ out,
-                                    int64_t rows, int64_t segs, int m, int u, int64_t n_rg) {
+                                    int64_t rows, int64_t segs, int m, int u, int64_t n_rg,
+                                    int nib) {
     const int64_t total = (int64_t)m * rows * segs;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -170,7 +212,7 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed,
             const int64_t seg = i % segs;
             const int64_t r = (i / segs) % rows;
             const int64_t t = i / (segs * rows);
-            out[i] = packed[packed_index(t, r, seg, m, u, n_rg)];
+            out[i] = (uint16_t)packed_code(packed, t, r, seg, m, u, n_rg, nib != 0);
         }
     }
 }
@@ -237,7 +279,10 @@ struct FusedShape {
     static constexpr int kXFloats = U * 8 * kXQF;
     static constexpr int kPsumBytes = 4 * kPsumFloats;
     static constexpr int kXBytes = 4 * kXFloats;
-    static constexpr int kTileBytes = M * U * 512;  // codes per (slice, row group)
+    static constexpr bool kNib = KB == 4;  // 16-entry tables: two codes per byte
+    static constexpr int kTileBytes = M * U * (kNib ? 256 : 512);  // codes per (slice, row group)
+    static constexpr int kLaneBytes = (kNib && U == 1) ? 8 : 16;   // lane offset in a chunk
+    static constexpr int kChunkBytes = (kNib && U == 1) ? 256 : 512;
     static constexpr int kXPerThread = (V * kSliceSegs + kThreads - 1) / kThreads;
     static constexpr int kCPT = kCodes / (4 * kWarps) > 0 ? kCodes / (4 * kWarps) : 1;
     static constexpr bool kFullCodes = kCPT * 4 * kWarps == kCodes;
@@ -577,10 +622,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // ---------------------------------------------------------------------------
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ void load_tile(uint4 (&cw)[M][U], const uint8_t* tp) {
+    using S = FusedShape<V, M, U, KB>;
+    if constexpr (!S::kNib) {
 #pragma unroll
-    for (int t = 0; t < M; ++t)
+        for (int t = 0; t < M; ++t)
 #pragma unroll
-        for (int c = 0; c < U; ++c) cw[t][c] = ldg_stream_v4(tp + (t * U + c) * 512);
+            for (int c = 0; c < U; ++c) cw[t][c] = ldg_stream_v4(tp + (t * U + c) * 512);
+    } else if constexpr (U == 1) {  // 8 bytes per lane and codebook
+#pragma unroll
+        for (int t = 0; t < M; ++t) {
+            uint2 v;
+            asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                         : "=r"(v.x), "=r"(v.y)
+                         : "l"(tp + t * 256));
+            cw[t][0] = make_uint4(v.x, v.y, 0u, 0u);
+        }
+    } else {  // U/2 chunks of 16 bytes per lane and codebook
+#pragma unroll
+        for (int t = 0; t < M; ++t)
+#pragma unroll
+            for (int c = 0; c < U / 2; ++c) cw[t][c] = ldg_stream_v4(tp + (t * (U / 2) + c) * 512);
+    }
+}
+
+// the 32-bit word of code idx (bytes = codes), byte mode or nibble mode
+template <bool NIB, int U>
+__device__ __forceinline__ uint32_t code_word(const uint4 (&cw)[U], int idx) {
+    if constexpr (!NIB) {
+        return word_of(cw[idx >> 4], (idx >> 2) & 3);
+    } else {
+        const uint32_t w = word_of(cw[(idx >> 3) >> 2], (idx >> 3) & 3);
+        return (idx & 4) ? ((w >> 4) & 0x0f0f0f0fu) : (w & 0x0f0f0f0fu);
+    }
 }
 
 // lb0/lb1 = per-lane PRMT constants: byte0 = lane<<2 | half<<7, bytes 1-2 =
@@ -608,12 +681,12 @@ __device__ __forceinline__ float gather_row_group(const uint4 (&cw)[M][U], const
                 float2 v;
                 {
                     const int idx = i * U + uu;
-                    const uint32_t w = word_of(cw[t][idx >> 4], (idx >> 2) & 3);
+                    const uint32_t w = code_word<S::kNib, U>(cw[t], idx);
                     v.x = lds_f32(__byte_perm(w, lb, 0x6504u | ((uint32_t)(idx & 3) << 4)) + region);
                 }
                 {
                     const int idx = (i + 1) * U + uu;
-                    const uint32_t w = word_of(cw[t][idx >> 4], (idx >> 2) & 3);
+                    const uint32_t w = code_word<S::kNib, U>(cw[t], idx);
                     v.y = lds_f32(__byte_perm(w, lb, 0x6504u | ((uint32_t)(idx & 3) << 4)) + region);
                 }
                 s2 = (t == 0 && uu == 0) ? v : __fadd2_rn(s2, v);
@@ -989,7 +1062,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     //    where the task's range was bulk-prefetched) during the input wait
     //    and the table build
     const int my_rgs = rg0 + warp < rg1 ? (int)((rg1 - rg0 - warp + kWarps - 1) / kWarps) : 0;
-    const uint8_t* cptr = tiles + (rg0 + warp) * S::kTileBytes + lane * 16;
+    const uint8_t* cptr = tiles + (rg0 + warp) * S::kTileBytes + lane * S::kLaneBytes;
     constexpr int64_t kStep = (int64_t)kWarps * S::kTileBytes;
     uint4 tb[D][M][U];
 #pragma unroll
@@ -1089,7 +1162,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
                 const int i = i0 + d;
                 if (i < n_rgs) {
                     if (pf > 0 && lane == 0 && i + pf < load_rgs)
-                        prefetch_l2_bulk(cptr - lane * 16 + (i + pf) * kStep, S::kTileBytes);
+                        prefetch_l2_bulk(cptr - lane * S::kLaneBytes + (i + pf) * kStep, S::kTileBytes);
                     const float v = gather_row_group<V, M, U, KB>(tb[d], sp0 + i * sstep, lb0, lb1,
                                                                   mask, early);
                     if (i + D < load_rgs) load_tile<V, M, U, KB>(tb[d], cptr + (i + D) * kStep);
@@ -1555,7 +1628,8 @@ __global__ void strict_gemm_kernel(const uint8_t* __restrict__ packed,
                                    const uint16_t* __restrict__ scales,
                                    const uint16_t* __restrict__ x, float* __restrict__ y,
                                    int64_t rows, int64_t segs, int v, int m, int kcount,
-                                   int64_t groups, int64_t g_eff, int n, int u, int64_t n_rg) {
+                                   int64_t groups, int64_t g_eff, int n, int u, int64_t n_rg,
+                                   int nib) {
     pdl_wait();
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= rows * n) return;
@@ -1566,7 +1640,7 @@ __global__ void strict_gemm_kernel(const uint8_t* __restrict__ packed,
         float seg_sum = 0.0f;
         for (int t = 0; t < m; ++t) {
             const uint32_t code = raw16 ? raw16[((int64_t)t * rows + r) * segs + seg]
-                                        : packed[packed_index(t, r, seg, m, u, n_rg)];
+                                        : packed_code(packed, t, r, seg, m, u, n_rg, nib != 0);
             const uint16_t* c = books + ((int64_t)t * kcount + code) * v;
             const uint16_t* xs = x + seg * v * (int64_t)n + col;
             float psum = 0.0f;
@@ -1770,7 +1844,7 @@ cudaError_t launch_prepack_codes(const Plan& p, const uint16_t* raw, uint8_t* pa
                                  unsigned* bad, cudaStream_t s) {
     const int64_t total = p.code_bytes;
     prepack_codes_kernel<<<grid_for(total, 256), 256, 0, s>>>(
-        raw, packed, total, p.rows, p.segs, p.m, p.u, p.n_rg, 1u << p.b, bad);
+        raw, packed, total, p.rows, p.segs, p.m, p.u, p.n_rg, 1u << p.b, bad, p.kbits == 4);
     return cudaGetLastError();
 }
 
@@ -1793,7 +1867,7 @@ cudaError_t launch_unpack_codes(const Plan& p, const uint8_t* packed, const uint
                                 uint16_t* out, cudaStream_t s) {
     const int64_t total = (int64_t)p.m * p.rows * p.segs;
     unpack_codes_kernel<<<grid_for(total, 256), 256, 0, s>>>(packed, raw16, out, p.rows, p.segs,
-                                                            p.m, p.u, p.n_rg);
+                                                            p.m, p.u, p.n_rg, p.kbits == 4);
     return cudaGetLastError();
 }
 
@@ -1818,7 +1892,7 @@ cudaError_t launch_strict_gemm(const Plan& p, const uint8_t* packed, const uint1
     const int64_t blocks = (total + threads - 1) / threads;
     strict_gemm_kernel<<<(unsigned)blocks, threads, 0, s>>>(
         packed, raw16, books, scales, x, y, p.rows, p.segs, p.v, p.m, p.kcount, p.groups,
-        p.g_eff, n, p.u, p.n_rg);
+        p.g_eff, n, p.u, p.n_rg, p.kbits == 4);
     return cudaGetLastError();
 }
 

@@ -15,7 +15,9 @@ import torch  # noqa: E402
 import paper_2512_17970_b200 as cg  # noqa: E402
 from oracle import codegemm_oracle as orc  # noqa: E402
 
-CONFIGS = {"m1v4g128": dict(v=4, m=1, b=8, g=128), "m2v8g128": dict(v=8, m=2, b=8, g=128)}
+CONFIGS = {"m1v4g128": dict(v=4, m=1, b=8, g=128), "m2v8g128": dict(v=8, m=2, b=8, g=128),
+           "m1v2b4g128": dict(v=2, m=1, b=4, g=128), "m2v4b4g128": dict(v=4, m=2, b=4, g=128),
+           "m1v4b6g128": dict(v=4, m=1, b=6, g=128)}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--rows", type=int, default=14336)
