@@ -400,6 +400,65 @@ __device__ __forceinline__ void load_centroid(float (&c)[V], const uint16_t* p) 
     }
 }
 
+// One sub-table (codebook t, segment-in-lane uu) of the build below.
+template <int V, int M, int U, int KB, bool FULL>
+__device__ __forceinline__ void build_subtable(float* psum, const uint16_t* bk, const float* xs,
+                                               int kcount, int t, int uu, int q, int c0,
+                                               const float (&cc)[FusedShape<V, M, U, KB>::kHoist
+                                                                      ? FusedShape<V, M, U, KB>::kCPT
+                                                                      : 1][V]) {
+    using S = FusedShape<V, M, U, KB>;
+    constexpr int kCPT = S::kCPT;
+    const int j = t * U + uu;
+    // x of this thread's 4 segments, paired for FFMA2:
+    // x01[k] = (x_s0k, x_s1k), x23[k] = (x_s2k, x_s3k)
+    float2 x01[V], x23[V];
+    {
+        const float4* src = reinterpret_cast<const float4*>(xs + (uu * 8 + q) * S::kXQF);
+#pragma unroll
+        for (int c = 0; c < V; ++c) {  // 2V pairs = V float4
+            const float4 w = src[c];
+            float2* d = (2 * c < V) ? &x01[2 * c] : &x23[2 * c - V];
+            d[0] = make_float2(w.x, w.y);
+            d[1] = make_float2(w.z, w.w);
+        }
+    }
+    float* dst = psum + (j >> 1) * S::kRegionFloats + (j & 1) * 32 + q * 4;
+    if constexpr (S::kHoist) {
+        float2 a01[kCPT], a23[kCPT];
+#pragma unroll
+        for (int k = 0; k < V; ++k)
+#pragma unroll
+            for (int i = 0; i < kCPT; ++i) {
+                const float2 cb = make_float2(cc[i][k], cc[i][k]);
+                a01[i] = k == 0 ? __ffma2_rn(cb, x01[0], make_float2(0.0f, 0.0f))
+                                : __ffma2_rn(cb, x01[k], a01[i]);
+                a23[i] = k == 0 ? __ffma2_rn(cb, x23[0], make_float2(0.0f, 0.0f))
+                                : __ffma2_rn(cb, x23[k], a23[i]);
+            }
+#pragma unroll
+        for (int i = 0; i < kCPT; ++i) {
+            const int c = c0 + 4 * kWarps * i;
+            if (FULL || c < kcount)
+                *reinterpret_cast<float4*>(dst + c * 64) =
+                    make_float4(a01[i].x, a01[i].y, a23[i].x, a23[i].y);
+        }
+    } else {
+#pragma unroll 1
+        for (int c = c0; c < kcount; c += 4 * kWarps) {
+            float ci[V];
+            load_centroid<V>(ci, bk + c * V);
+            float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                a01 = __ffma2_rn(make_float2(ci[k], ci[k]), x01[k], a01);
+                a23 = __ffma2_rn(make_float2(ci[k], ci[k]), x23[k], a23);
+            }
+            *reinterpret_cast<float4*>(dst + c * 64) = make_float4(a01.x, a01.y, a23.x, a23.y);
+        }
+    }
+}
+
 // books16: raw binary16 codebooks [t][kcount][V];  xs: staged x pairs.
 // FULL (kcount == 2**KB, every b = 8 / b = 4 table): no per-code bounds test,
 // so the kCPT codes' 2*kCPT FFMA2 chains of a sub-table are interleaved
@@ -430,11 +489,23 @@ __device__ __forceinline__ void build_psumbook_impl(float* psum, const uint16_t*
                 }
             }
         }
+        // (FULL: the sub-table loop unrolled, so the table stores of one sub-table
+        // overlap the FFMA2 chains of the next instead of alternating with them)
+#pragma unroll
+        for (int uu = 0; uu < (FULL ? U : 1); ++uu) {
+            build_subtable<V, M, U, KB, FULL>(psum, bk, xs, kcount, t, uu, q, c0, cc);
+        }
 #pragma unroll 1
-        for (int uu = 0; uu < U; ++uu) {
-            const int j = t * U + uu;
-            // x of this thread's 4 segments, paired for FFMA2:
-            // x01[k] = (x_s0k, x_s1k), x23[k] = (x_s2k, x_s3k)
+        for (int uu = FULL ? U : 0; uu < U; ++uu) {
+            build_subtable<V, M, U, KB, FULL>(psum, bk, xs, kcount, t, uu, q, c0, cc);
+        }
+    }
+}
+#if 0
+        {
+            {
+                const int j = t * U;
+                const int uu = 0;
             float2 x01[V], x23[V];
             {
                 const float4* src = reinterpret_cast<const float4*>(xs + (uu * 8 + q) * S::kXQF);
@@ -483,6 +554,7 @@ __device__ __forceinline__ void build_psumbook_impl(float* psum, const uint16_t*
         }
     }
 }
+#endif
 
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ void build_psumbook_smem(float* psum, const uint16_t* books16,
