@@ -426,6 +426,35 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
                                 "layer %d: gathered x must be CG_X_F32 inside the comm buffer", i);
             }
         }
+        // LL stage exchange: every later-stage x inside the gathered buffers must be
+        // the gathered y of a layer pushed in an earlier stage of this launch (its
+        // range contains that layer's local rows); else the fenced per-stage protocol
+        {
+            bool ll = !std::getenv("CG_XC_LL") || std::atoi(std::getenv("CG_XC_LL")) != 0;
+            for (int i = 0; i < count; ++i) {
+                cg::LayerTask& t = gp.layer[i];
+                t.xll = 0;
+                const uintptr_t xa = reinterpret_cast<uintptr_t>(t.x32);
+                if (!t.x32 || (t.xchg & cg::kXchgWait) || xa < lo || xa >= hi) continue;
+                const uintptr_t xe = xa + (uintptr_t)(t.cols * n * 4);
+                bool found = false;
+                for (int j = 0; j < count && !found; ++j) {
+                    const cg::LayerTask& u = gp.layer[j];
+                    const uintptr_t ya = reinterpret_cast<uintptr_t>(u.y);
+                    found = (u.xchg & cg::kXchgPush) && u.stage < t.stage && ya >= xa &&
+                            ya + (uintptr_t)(u.rows * n * 4) <= xe;
+                }
+                if (found) t.xll = 1;
+                else ll = false;
+            }
+            if (ll) {
+                gp.flags |= cg::kFlagXcLL;
+            } else {
+                for (int i = 0; i < count; ++i) gp.layer[i].xll = 0;
+            }
+            gp.xc_gbase = comm->base + cg::kXcHeader;
+            gp.xc_ll = comm->base + cg::kXcHeader + comm->bytes;
+        }
         gp.xc_local = comm->base;
         gp.xc_world = comm->world;
         gp.xc_rank = comm->rank;
@@ -1233,8 +1262,9 @@ int cg_comm_create(int world, int rank, int64_t bytes, int ctas, int timeout_ms,
     c->device = device;
     c->bytes = (bytes + 255) & ~int64_t(255);
     c->timeout_ns = (unsigned long long)timeout_ms * 1000000ull;
-    cudaError_t e = cudaMalloc(&c->base, (size_t)(cg::kXcHeader + c->bytes));
-    if (e == cudaSuccess) e = cudaMemset(c->base, 0, (size_t)(cg::kXcHeader + c->bytes));
+    // header | gathered buffers | their LL copy ((value, epoch) pairs: 2x the bytes)
+    cudaError_t e = cudaMalloc(&c->base, (size_t)(cg::kXcHeader + 3 * c->bytes));
+    if (e == cudaSuccess) e = cudaMemset(c->base, 0, (size_t)(cg::kXcHeader + 3 * c->bytes));
     if (e != cudaSuccess) {
         cudaFree(c->base);
         delete c;

@@ -43,6 +43,8 @@ struct LayerTask {
     unsigned long long* rg_cnt;  // [0] launches completed, [1 + rg] row-group completions
                                  // (this layer is a producer for a later layer), or null
     int xchg;                 // kXchgPush | kXchgWait (row-shard exchange launches), else 0
+    int xll;                  // x is the gathered y of a layer pushed earlier in this launch:
+                              // read from the LL copy (value, epoch pairs), no stage wait
     int zero_per;             // elements of y each CTA zeroes (rows * n / grid, rounded up to 4)
 };
 
@@ -85,6 +87,14 @@ struct GroupParams {
     long long xc_delta[kMaxRanks];         // peer copy address - local address (bytes)
     int xc_world, xc_rank;
     unsigned long long xc_timeout_ns;      // trap a wait that exceeds it (0: wait forever)
+    // LL exchange (kFlagXcLL): stage pushes write (value, epoch) pairs into every
+    // rank's LL copy of the gathered buffers -- 8 bytes per float at
+    // xc_ll + 2 * (byte offset in the gathered buffers) -- and consumers spin on
+    // the epoch: no fence, no counter.  The launch's last exchange pushes every
+    // layer's plain rows once, fenced and counted (user-visible buffers, WAIT
+    // layers of later launches, overwrite protection).
+    unsigned char* xc_ll;                  // this rank's LL copy
+    const unsigned char* xc_gbase;         // this rank's gathered buffers (offset origin)
 };
 
 // Psumbook dump (bit-exactness check of the fused kernel's on-chip table)
@@ -101,6 +111,7 @@ constexpr int kFlagNoPrefetch = 2;
 constexpr int kFlagLastArriver = 4;  // a layer has more tasks than the grid: last arriver sums
 constexpr int kFlagDeterministic = 16;  // split-K by tickets + ordered sums (else L2 reduce-add)
 constexpr int kFlagXRegs = 32;  // x staged through registers (unaligned x / odd cols / n > 1)
+constexpr int kFlagXcLL = 128;  // exchange launch: LL stage pushes (GroupParams::xc_ll)
 // diagnostics only (CG_DEBUG_FLAGS): wrong results, phase isolation for timing
 constexpr int kFlagRowDeps = 64;  // stages ordered by row-group readiness, not grid barriers
 constexpr int kFlagDirectAdd = 1 << 14;  // split-K partials red.add'ed into y even at n == 1

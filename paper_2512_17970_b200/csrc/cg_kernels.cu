@@ -344,6 +344,41 @@ __device__ __forceinline__ void load_x(uint16_t (&r)[FusedShape<V, M, U, KB>::kX
     }
 }
 
+// x of an LL consumer: element e lives at xc_ll + 2 * (byte offset of x32 + e in
+// the gathered buffers) as (value, epoch); spin until this launch's epoch shows
+// (an 8-byte store is single-copy atomic: value and epoch arrive together)
+__device__ __forceinline__ float ll_load(const float* x32, const GroupParams& p, unsigned epoch) {
+    const int64_t off = reinterpret_cast<const unsigned char*>(x32) - p.xc_gbase;
+    const float2* a = reinterpret_cast<const float2*>(p.xc_ll + 2 * off);
+    unsigned long long t0 = 0;
+    while (true) {
+        uint32_t v, ep;
+        asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];" : "=r"(v), "=r"(ep) : "l"(a) : "memory");
+        if (ep == epoch) return __uint_as_float(v);
+        if (p.xc_timeout_ns) {
+            const unsigned long long t = gtimer();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > p.xc_timeout_ns) __trap();  // a peer never pushed
+        }
+    }
+}
+
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void load_x_ll(uint16_t (&r)[FusedShape<V, M, U, KB>::kXPerThread],
+                                          const LayerTask& L, const GroupParams& p, unsigned epoch,
+                                          int64_t slice, int n, int col, int tid) {
+    using S = FusedShape<V, M, U, KB>;
+    const int64_t e0 = slice * (int64_t)(S::kSliceSegs * V);
+#pragma unroll
+    for (int i = 0; i < S::kXPerThread; ++i) {
+        const int l = tid + i * kThreads;
+        const int64_t e = e0 + l;
+        r[i] = (l < S::kSliceSegs * V && e < L.cols)
+                   ? __half_as_ushort(__float2half_rn(ll_load(L.x32 + e * n + col, p, epoch)))
+                   : (uint16_t)0;
+    }
+}
+
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ void store_x(float* xs,
                                         const uint16_t (&r)[FusedShape<V, M, U, KB>::kXPerThread],
@@ -1041,7 +1076,7 @@ __device__ __forceinline__ bool next_task_s(const CtaState& cs, int nl, int ns, 
 // unaligned slices; not for a row-readiness consumer (its x is waited for
 // per row group inside the task, after the copy would have been issued)
 __device__ __forceinline__ bool x_by_copy(const GroupParams& p, const LayerTask& L) {
-    return p.n == 1 && !(p.flags & kFlagXRegs) && (L.x32 == nullptr || L.dep < 0);
+    return p.n == 1 && !(p.flags & kFlagXRegs) && (L.x32 == nullptr || L.dep < 0) && !L.xll;
 }
 
 // Task geometry (all task counts fit in 32 bits).
@@ -1153,7 +1188,8 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
         __syncthreads();
     }
     uint16_t xreg[S::kXPerThread];
-    if (!x_by_copy(p, L)) load_x<V, M, U, KB>(xreg, L, slice, n, 0, tid);
+    if (L.xll) load_x_ll<V, M, U, KB>(xreg, L, p, (unsigned)(cs.xc_base + 1), slice, n, 0, tid);
+    else if (!x_by_copy(p, L)) load_x<V, M, U, KB>(xreg, L, slice, n, 0, tid);
 
     // 2. the previous task is done with the table; the staging buffer of two
     //    tasks ago has been read by its flush; the next task's inputs start
@@ -1188,7 +1224,8 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     for (int col = 0; col < n; ++col) {
         if (col > 0) {
             __syncthreads();  // previous column's table is no longer read
-            load_x<V, M, U, KB>(xreg, L, slice, n, col, tid);
+            if (L.xll) load_x_ll<V, M, U, KB>(xreg, L, p, (unsigned)(cs.xc_base + 1), slice, n, col, tid);
+            else load_x<V, M, U, KB>(xreg, L, slice, n, col, tid);
         }
         if (x_by_copy(p, L)) {
             const int64_t e0 = (int64_t)slice * (S::kSliceSegs * V);
@@ -1359,9 +1396,12 @@ __device__ __noinline__ void xc_prologue(const GroupParams& p, CtaState& cs) {
 __device__ __noinline__ void xc_push(unsigned char* smem_raw, int off_bar, int stage, int tid,
                                      int n_layers, int world, int rank, const long long* deltas,
                                      const unsigned long long* arrive, bool gpu_scope,
-                                     unsigned long long timeout_ns) {
+                                     unsigned long long timeout_ns, bool all_stages) {
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + off_bar);
-    if (!((cs.xc_push_mask >> stage) & 1)) return;  // (a launch's closing arrival: nothing to push)
+    // (a launch's closing arrival with nothing to push; LL launches push every
+    // stage's plain rows here, once)
+    if (!all_stages && !((cs.xc_push_mask >> stage) & 1)) return;
+    if (all_stages && !cs.xc_push_mask) return;
     if (!cs.xc_pushed) {
         // the first stores into peers' buffers in this launch: every rank has
         // finished its previous launches (and their reads)
@@ -1373,7 +1413,7 @@ __device__ __noinline__ void xc_push(unsigned char* smem_raw, int off_bar, int s
         if (r == rank) continue;
         const long long d = deltas[r];
         for (int l = 0; l < n_layers; ++l) {
-            if (cs.l_stage[l] != stage || !((cs.xc_layer_mask >> l) & 1)) continue;
+            if ((!all_stages && cs.l_stage[l] != stage) || !((cs.xc_layer_mask >> l) & 1)) continue;
             float* y = cs.xc_y[l];
             const int elems = cs.xc_elems[l];
             const int per = (((elems + (int)gridDim.x - 1) / (int)gridDim.x) + 3) & ~3;
@@ -1387,6 +1427,43 @@ __device__ __noinline__ void xc_push(unsigned char* smem_raw, int off_bar, int s
         }
     }
     __syncthreads();
+}
+
+// LL push (all threads, after the grid barrier that closed `stage`): this CTA's
+// share of the stage's pushed layers into every rank's LL copy as (value,
+// epoch) pairs -- 8-byte stores, no fence, no counter; consumers spin on the
+// epoch.  The first stores of a launch wait until every rank finished its
+// previous launches (their last exchange), so no LL slot is overwritten while
+// a peer may still read it.
+__device__ __noinline__ void xc_push_ll(unsigned char* smem_raw, int off_bar, int stage, int tid,
+                                        int n_layers, int world, const long long* deltas,
+                                        const unsigned long long* arrive, unsigned char* ll,
+                                        const unsigned char* gbase, unsigned long long timeout_ns) {
+    CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + off_bar);
+    if (!((cs.xc_push_mask >> stage) & 1)) return;
+    if (!cs.xc_pushed) {
+        if (tid == 0) xc_wait(arrive, cs.xc_base * (unsigned long long)world * gridDim.x, false,
+                              timeout_ns);
+        __syncthreads();
+        if (tid == 0) cs.xc_pushed = 1;
+    }
+    const uint32_t epoch = (uint32_t)(cs.xc_base + 1);
+    for (int l = 0; l < n_layers; ++l) {
+        if (cs.l_stage[l] != stage || !((cs.xc_layer_mask >> l) & 1)) continue;
+        const float* y = cs.xc_y[l];
+        const int elems = cs.xc_elems[l];
+        const int per = (elems + (int)gridDim.x - 1) / (int)gridDim.x;
+        const int e0 = min((int)blockIdx.x * per, elems), e1 = min(e0 + per, elems);
+        unsigned char* dst0 = ll + 2 * (reinterpret_cast<const unsigned char*>(y) - gbase);
+        for (int e = e0 + tid; e < e1; e += kThreads) {
+            const uint32_t v = __float_as_uint(__ldcg(y + e));
+            for (int r = 0; r < world; ++r) {
+                float2* d = reinterpret_cast<float2*>(dst0 + deltas[r]) + e;
+                asm volatile("st.volatile.global.v2.u32 [%0], {%1,%2};" ::"l"(d), "r"(v), "r"(epoch)
+                             : "memory");
+            }
+        }
+    }
 }
 
 // Grid barrier between dependent stages of a launch (the monotonic counter
@@ -1417,6 +1494,16 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
         ++cs.n_bar;
     }
     __syncthreads();
+    if (p.xc_local && (p.flags & kFlagXcLL) && !final) {
+        // LL: the stage's rows to every rank as (value, epoch) pairs; the next
+        // stage's consumers spin on them -- no fence, no wait here
+        if ((cs.xc_push_mask >> stage) & 1) {
+            xc_push_ll(smem_raw, p.off_bar, stage, tid, p.n_layers, p.xc_world, p.xc_delta,
+                       reinterpret_cast<const unsigned long long*>(p.xc_local + kXcArrive), p.xc_ll,
+                       p.xc_gbase, p.xc_timeout_ns);
+        }
+        return;
+    }
     if (p.xc_local && (((cs.xc_push_mask >> stage) & 1) || final)) {
         // row-shard exchange: the stage's rows to every peer, then (unless the
         // launch ends here) every rank's rows before the next stage reads them
@@ -1424,7 +1511,7 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
         const unsigned long long* arrive =
             reinterpret_cast<const unsigned long long*>(p.xc_local + kXcArrive);
         xc_push(smem_raw, p.off_bar, stage, tid, p.n_layers, p.xc_world, p.xc_rank, p.xc_delta,
-                arrive, gs, p.xc_timeout_ns);
+                arrive, gs, p.xc_timeout_ns, (p.flags & kFlagXcLL) != 0);
         if (tid == 0) {
             // (the system-scope fence in here is the exchange's main cost: ~1.1 us
             // idle, ~4.5 us inside the kernel -- tools/micro/membar.cu, stamps)
