@@ -282,7 +282,6 @@ struct FusedShape {
     static constexpr bool kNib = KB == 4;  // 16-entry tables: two codes per byte
     static constexpr int kTileBytes = M * U * (kNib ? 256 : 512);  // codes per (slice, row group)
     static constexpr int kLaneBytes = (kNib && U == 1) ? 8 : 16;   // lane offset in a chunk
-    static constexpr int kChunkBytes = (kNib && U == 1) ? 256 : 512;
     static constexpr int kXPerThread = (V * kSliceSegs + kThreads - 1) / kThreads;
     static constexpr int kCPT = kCodes / (4 * kWarps) > 0 ? kCodes / (4 * kWarps) : 1;
     static constexpr bool kFullCodes = kCPT * 4 * kWarps == kCodes;
@@ -591,10 +590,85 @@ __device__ __forceinline__ void build_psumbook_impl(float* psum, const uint16_t*
 }
 #endif
 
+#ifdef CG_BUILD_R01
+template <int V>
+__device__ __forceinline__ void psum_entries(float* dst, const float (&cc)[V],
+                                             const float2 (&x01)[V], const float2 (&x23)[V]) {
+    float2 a01 = make_float2(0.0f, 0.0f), a23 = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        a01 = __ffma2_rn(make_float2(cc[k], cc[k]), x01[k], a01);
+        a23 = __ffma2_rn(make_float2(cc[k], cc[k]), x23[k], a23);
+    }
+    *reinterpret_cast<float4*>(dst) = make_float4(a01.x, a01.y, a23.x, a23.y);
+}
+
+// (CG_BUILD_R01: the round-1 build, per-code bounds tests, for A/B timing)
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void build_psumbook_r01(float* psum, const uint16_t* books16,
+                                                    const float* xs, int kcount, int tid) {
+    using S = FusedShape<V, M, U, KB>;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int q = lane & 7;      // this thread writes lanes 4q..4q+3 of a code row
+    const int csub = lane >> 3;  // 4 codes per warp per pass
+    const int c0 = csub + 4 * warp;
+    constexpr int kCPT = S::kCPT;
+    const bool full = S::kFullCodes && kcount == S::kCodes;
+#pragma unroll 1
+    for (int t = 0; t < M; ++t) {
+        const uint16_t* bk = books16 + t * kcount * V;
+        float cc[S::kHoist ? kCPT : 1][V];
+        if constexpr (S::kHoist) {
+#pragma unroll
+            for (int i = 0; i < kCPT; ++i) {
+                const int c = c0 + 4 * kWarps * i;
+                if (full || c < kcount) load_centroid<V>(cc[i], bk + c * V);
+            }
+        }
+#pragma unroll 1
+        for (int uu = 0; uu < U; ++uu) {
+            const int j = t * U + uu;
+            // x of this thread's 4 segments, paired for FFMA2:
+            // x01[k] = (x_s0k, x_s1k), x23[k] = (x_s2k, x_s3k)
+            float2 x01[V], x23[V];
+            {
+                const float4* src = reinterpret_cast<const float4*>(xs + (uu * 8 + q) * S::kXQF);
+#pragma unroll
+                for (int c = 0; c < V; ++c) {  // 2V pairs = V float4
+                    const float4 w = src[c];
+                    float2* d = (2 * c < V) ? &x01[2 * c] : &x23[2 * c - V];
+                    d[0] = make_float2(w.x, w.y);
+                    d[1] = make_float2(w.z, w.w);
+                }
+            }
+            float* dst = psum + (j >> 1) * S::kRegionFloats + (j & 1) * 32 + q * 4;
+            if constexpr (S::kHoist) {
+#pragma unroll
+                for (int i = 0; i < kCPT; ++i) {
+                    const int c = c0 + 4 * kWarps * i;
+                    if (full || c < kcount) psum_entries<V>(dst + c * 64, cc[i], x01, x23);
+                }
+            } else {
+#pragma unroll 1
+                for (int c = c0; c < kcount; c += 4 * kWarps) {
+                    float ci[V];
+                    load_centroid<V>(ci, bk + c * V);
+                    psum_entries<V>(dst + c * 64, ci, x01, x23);
+                }
+            }
+        }
+    }
+}
+
+#endif
+
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ void build_psumbook_smem(float* psum, const uint16_t* books16,
                                                     const float* xs, int kcount, int tid) {
     using S = FusedShape<V, M, U, KB>;
+#ifdef CG_BUILD_R01
+    return build_psumbook_r01<V, M, U, KB>(psum, books16, xs, kcount, tid);
+#endif
     if (S::kFullCodes && kcount == S::kCodes)
         build_psumbook_impl<V, M, U, KB, true>(psum, books16, xs, kcount, tid);
     else
@@ -1261,6 +1335,12 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
             if (tid == 0) cs.zero_ready = 1;
         }
         int64_t row = (rg0 + warp) * 16 + mask;
+        // the output store of a row group, one predicated instruction per mode (no
+        // generic-address branches in the loop: they split it into basic blocks the
+        // scheduler cannot interleave): smem staging, red.add into y, or plain store
+        const int64_t rows_l = L.rows;
+        const uint32_t out_s = stage_out ? smem_u32(out) : 0u;
+        const int out_mode = stage_out ? 1 : (direct ? 2 : 0);
         // D-deep register pipeline: tile i+D is requested as soon as tile i is consumed
         const int n_rgs = (p.flags & kFlagDbgSkipGather) ? 0 : my_rgs;
         const int pf = (p.flags & kFlagNoPrefetch) ? 0 : p.pf_dist;
@@ -1275,9 +1355,21 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
                     const float v = gather_row_group<V, M, U, KB>(tb[d], sp0 + i * sstep, lb0, lb1,
                                                                   mask, early);
                     if (i + D < load_rgs) load_tile<V, M, U, KB>(tb[d], cptr + (i + D) * kStep);
-                    if (lane < 16 && row < L.rows) {
-                        if (direct) atomicAdd(out + row * n + col, v);  // (RED, result unused)
-                        else out[row * n + col] = v;
+                    {
+                        const bool w = lane < 16 && row < rows_l;
+                        const int64_t o = row * n + col;
+                        asm volatile(
+                            "{\n\t.reg .pred pw, pg, ps, pr;\n\t"
+                            "setp.ne.s32 pw, %3, 0;\n\t"
+                            "setp.eq.and.s32 pg, %2, 0, pw;\n\t"
+                            "setp.eq.and.s32 ps, %2, 1, pw;\n\t"
+                            "setp.eq.and.s32 pr, %2, 2, pw;\n\t"
+                            "@pg st.global.f32 [%0], %4;\n\t"
+                            "@ps st.shared.f32 [%1], %4;\n\t"
+                            "@pr red.global.add.f32 [%0], %4;\n\t}"
+                            ::"l"(out + o), "r"(out_s + (uint32_t)(o * 4)), "r"(out_mode),
+                            "r"((int)w), "f"(v)
+                            : "memory");
                     }
                     row += row_step;
                 }
