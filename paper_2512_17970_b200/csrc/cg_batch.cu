@@ -466,6 +466,8 @@ __global__ void __launch_bounds__(BWarps<NT>::kThreads, 1)
         if (one_scale) close_group(0);
         // ---- CTA sum of the 8 warp partials (warp order: deterministic)
         constexpr int kCols = NT * 8;
+        constexpr int kRed = kCols + 2;  // row stride of the partials (+8 B: rows g, g+8 in
+                                         // different banks; keeps float2 alignment)
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(BWarps<NT>::kThreads, 1)
                 for (int h = 0; h < 2; ++h) {
                     const int row = mt * 16 + g + 8 * h;
                     const int col = nt * 8 + 2 * tq;
-                    *reinterpret_cast<float2*>(red + (warp * 32 + row) * kCols + col) =
+                    *reinterpret_cast<float2*>(red + (warp * 32 + row) * kRed + col) =
                         make_float2(tot[mt][nt][2 * h], tot[mt][nt][2 * h + 1]);
                 }
         __syncthreads();
@@ -485,9 +487,9 @@ __global__ void __launch_bounds__(BWarps<NT>::kThreads, 1)
             const int row = e / kCols, col = e - (e / kCols) * kCols;
             const int64_t grow = (int64_t)k.rset * 32 + row;
             if (col >= n || grow >= L.rows) continue;
-            float a = red[row * kCols + col];
+            float a = red[row * kRed + col];
 #pragma unroll
-            for (int w = 1; w < kBatchWarps; ++w) a += red[(w * 32 + row) * kCols + col];
+            for (int w = 1; w < kBatchWarps; ++w) a += red[(w * 32 + row) * kRed + col];
             out[grow * ldo + col] = a;
         }
         __syncthreads();  // red and this buffer are free for the next task
@@ -584,7 +586,7 @@ int batch_layout(int v, int m, int kcount, int nt, int ks_chunks, int gis, Batch
     const int tile = ks_chunks * m * batch_code_unit(v);  // one row tile's codes of a task
     const int codes = 2 * tile;
     const int scl = gis * 64;
-    const int red = (nt == 4 ? 8 : 16) * 32 * nt * 8 * 4;  // warps x 32 rows x columns
+    const int red = (nt == 4 ? 8 : 16) * 32 * (nt * 8 + 2) * 4;  // warps x 32 rows x padded columns
     int o = 0;
     const int off_tbl = o;
     o += up(tbl);
