@@ -684,6 +684,19 @@ __device__ __forceinline__ void build_psumbook_smem(float* psum, const uint16_t*
 // After the steps for masks 1,2,4,8 a lane holds the row
 // bit0*8 + bit1*4 + bit2*2 + bit3 summed over the 16 lanes sharing bit4.
 // ---------------------------------------------------------------------------
+// butterfly shuffle as inline PTX (every lane of the warp participates: the
+// gather loop is warp-uniform), so ptxas sees a plain SHFL rather than the
+// intrinsic's divergence-checked form
+__device__ __forceinline__ float shfl_bfly(float v, int mk) {
+#ifdef CG_SHFL_INTRINSIC
+    return __shfl_xor_sync(0xffffffffu, v, mk);
+#else
+    float r;
+    asm("shfl.sync.bfly.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=f"(r) : "f"(v), "r"(mk));
+    return r;
+#endif
+}
+
 // halving step on slot-permuted partials: keep slots [0, CNT/2), add the
 // partner's slots [CNT/2, CNT) (same rows, see row_mask)
 template <int CNT>
@@ -692,13 +705,13 @@ __device__ __forceinline__ void halve(float (&a)[16], int mk) {
     for (int i = 0; i < CNT / 2; i += 2) {
         if constexpr (CNT >= 4) {
             const float2 mine = make_float2(a[i], a[i + 1]);
-            const float2 other = make_float2(__shfl_xor_sync(0xffffffffu, a[i + CNT / 2], mk),
-                                             __shfl_xor_sync(0xffffffffu, a[i + 1 + CNT / 2], mk));
+            const float2 other = make_float2(shfl_bfly(a[i + CNT / 2], mk),
+                                             shfl_bfly(a[i + 1 + CNT / 2], mk));
             const float2 sum = __fadd2_rn(mine, other);
             a[i] = sum.x;
             a[i + 1] = sum.y;
         } else {
-            a[i] += __shfl_xor_sync(0xffffffffu, a[i + CNT / 2], mk);
+            a[i] += shfl_bfly(a[i + CNT / 2], mk);
         }
     }
 }
@@ -890,7 +903,7 @@ __device__ __forceinline__ float gather_row_group(const uint4 (&cw)[M][U], const
     halve<4>(a, 4);
     if (!early) apply_scales<2>(a, sp + (mask & ~1), mask & 1);
     halve<2>(a, 8);
-    a[0] += __shfl_xor_sync(0xffffffffu, a[0], 16);
+    a[0] += shfl_bfly(a[0], 16);
     return a[0];
 }
 
