@@ -241,6 +241,15 @@ int cg_stages_launch(cg_stages* plan, void* stream);
 int cg_stages_run_host(cg_stages* plan, const void* x_host, int64_t x_bytes, void* x_dev,
                        const void* y_dev, void* y_host, int64_t y_bytes, void* stream);
 int cg_stages_destroy(cg_stages* plan);
+/*
+ * Host mirrors of a prepared plan's outputs: host_ys[i] (pinned, device-mapped
+ * host memory such as cudaHostAlloc / torch pin_memory; NULL = none) receives
+ * layer i's y from the kernel itself once the layer's stage is complete, so the
+ * copies overlap the later stages and cg_stages_run_host needs no D2H copy
+ * (y_bytes = 0).  The last stage's copy costs one more grid barrier.  host_ys
+ * = NULL removes the mirrors.  Not for exchange plans.
+ */
+int cg_stages_set_mirror(cg_stages* plan, void* const* host_ys);
 
 /* Same with HOST buffers: copies x in, runs, copies y out, synchronises. */
 int cg_layer_gemm_host(cg_layer* layer, const uint16_t* x, int n, float* y, int mode,

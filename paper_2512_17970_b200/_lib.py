@@ -49,6 +49,7 @@ EXPORTS = (
     "cg_stages_prepare",
     "cg_stages_launch",
     "cg_stages_run_host",
+    "cg_stages_set_mirror",
     "cg_stages_destroy",
     "cg_comm_create",
     "cg_comm_buffer",
@@ -62,6 +63,7 @@ EXPORTS = (
     "cg_layer_psumbook",
     "cg_layer_unpack_codes",
     "cg_psumbook_build",
+    "cg_psumbook_build_f32",
 )
 
 
@@ -151,6 +153,8 @@ def load() -> ctypes.CDLL:
     lib.cg_stages_launch.restype = i
     lib.cg_stages_run_host.argtypes = [vp, p, i64, p, p, p, i64, vp]
     lib.cg_stages_run_host.restype = i
+    lib.cg_stages_set_mirror.argtypes = [vp, ctypes.POINTER(vp)]
+    lib.cg_stages_set_mirror.restype = i
     lib.cg_stages_destroy.argtypes = [vp]
     lib.cg_stages_destroy.restype = i
     lib.cg_comm_create.argtypes = [i, i, ctypes.c_int64, i, i, i, ctypes.POINTER(vp)]

@@ -1147,6 +1147,17 @@ int cg_gemm_stages_xchg(cg_layer* const* layers, const void* const* xs, const in
 // ---- prepared staged launches (cg_stages_*): planned once, launched per call
 struct cg_stages {
     StagedPlan plan;
+    float* mirror[cg::kMaxGroup] = {nullptr};  // host-mapped y copies (cg_stages_set_mirror)
+    int gen = 0;  // bumped whenever the launch parameters change
+    // cg_stages_run_host replays one CUDA graph (H2D, the launch, D2H): a direct
+    // cooperative launch costs tens of microseconds of host time per call
+    cudaGraphExec_t gexec = nullptr;
+    int g_gen = -1;
+    const void* g_xh = nullptr;
+    void* g_xd = nullptr;
+    const void* g_yd = nullptr;
+    void* g_yh = nullptr;
+    int64_t g_xb = -1, g_yb = -1;
     int count = 0, n = 0, device = 0;
     cg_layer* layers[cg::kMaxGroup] = {nullptr};
     const uint16_t* xs[cg::kMaxGroup] = {nullptr};
@@ -1165,6 +1176,8 @@ int replan_if_needed(cg_stages* P) {
                          P->comm ? P->xchg : nullptr, P->comm, &P->plan);
     if (rc) return rc;
     for (int i = 0; i < P->count; ++i) P->ws[i] = P->layers[i]->ws;
+    for (int i = 0; i < P->count; ++i) P->plan.gp.layer[i].mirror = P->mirror[i];
+    ++P->gen;
     return CG_OK;
 }
 }  // namespace
@@ -1223,16 +1236,88 @@ int cg_stages_run_host(cg_stages* P, const void* x_host, int64_t x_bytes, void* 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int rc = replan_if_needed(P);
     if (rc) return rc;
-    if (x_bytes) CG_CUDA(cudaMemcpyAsync(x_dev, x_host, (size_t)x_bytes, cudaMemcpyHostToDevice, s),
-                         "x H2D");
-    if ((rc = launch_plan(P->plan, s))) return rc;
-    if (y_bytes) CG_CUDA(cudaMemcpyAsync(y_host, y_dev, (size_t)y_bytes, cudaMemcpyDeviceToHost, s),
-                         "y D2H");
+    const bool same = P->gexec && P->g_gen == P->gen && P->g_xh == x_host && P->g_xb == x_bytes &&
+                      P->g_xd == x_dev && P->g_yd == y_dev && P->g_yh == y_host && P->g_yb == y_bytes;
+    if (!same && !std::getenv("CG_NO_HOST_GRAPH")) {
+        // (re)capture: H2D of the inputs, the launch (no PDL inside a graph of its
+        // own), D2H of the outputs -- then every call is one graph launch
+        if (P->gexec) cudaGraphExecDestroy(P->gexec);
+        P->gexec = nullptr;
+        cudaStream_t cs = nullptr;
+        cudaGraph_t graph = nullptr;
+        bool ok = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            if (x_bytes)
+                ok = cudaMemcpyAsync(x_dev, x_host, (size_t)x_bytes, cudaMemcpyHostToDevice, cs) ==
+                     cudaSuccess;
+            StagedPlan sp = P->plan;
+            sp.pdl = false;
+            if (ok) ok = cg::launch_group_gemv(sp.v, sp.m, sp.u, sp.kbits, sp.gp, sp.grid, sp.smem,
+                                               false, cs) == cudaSuccess;
+            if (ok && y_bytes)
+                ok = cudaMemcpyAsync(y_host, y_dev, (size_t)y_bytes, cudaMemcpyDeviceToHost, cs) ==
+                     cudaSuccess;
+            ok = (cudaStreamEndCapture(cs, &graph) == cudaSuccess) && ok;
+            if (ok) ok = cudaGraphInstantiate(&P->gexec, graph, 0) == cudaSuccess;
+        }
+        if (graph) cudaGraphDestroy(graph);
+        if (cs) cudaStreamDestroy(cs);
+        if (!ok) {  // (capture unsupported here: direct calls below)
+            cudaGetLastError();
+            if (P->gexec) cudaGraphExecDestroy(P->gexec);
+            P->gexec = nullptr;
+        } else {
+            P->g_gen = P->gen;
+            P->g_xh = x_host;
+            P->g_xb = x_bytes;
+            P->g_xd = x_dev;
+            P->g_yd = y_dev;
+            P->g_yh = y_host;
+            P->g_yb = y_bytes;
+        }
+    }
+    if (P->gexec && P->g_gen == P->gen && P->g_xh == x_host && P->g_xb == x_bytes &&
+        P->g_xd == x_dev && P->g_yd == y_dev && P->g_yh == y_host && P->g_yb == y_bytes) {
+        CG_CUDA(cudaGraphLaunch(P->gexec, s), "staged host call (graph)");
+    } else {
+        if (x_bytes)
+            CG_CUDA(cudaMemcpyAsync(x_dev, x_host, (size_t)x_bytes, cudaMemcpyHostToDevice, s),
+                    "x H2D");
+        if ((rc = launch_plan(P->plan, s))) return rc;
+        if (y_bytes)
+            CG_CUDA(cudaMemcpyAsync(y_host, y_dev, (size_t)y_bytes, cudaMemcpyDeviceToHost, s),
+                    "y D2H");
+    }
     CG_CUDA(cudaStreamSynchronize(s), "staged host call");
     return CG_OK;
 }
 
+int cg_stages_set_mirror(cg_stages* P, void* const* host_ys) {
+    if (!P) return fail(CG_ERR_ARG, "NULL plan");
+    if (P->comm && host_ys) return fail(CG_ERR_ARG, "host mirrors are not supported on exchange plans");
+    DeviceGuard guard(P->device);
+    for (int i = 0; i < P->count; ++i) {
+        float* h = host_ys ? static_cast<float*>(host_ys[i]) : nullptr;
+        if (h) {
+            // pinned (page-locked) host memory, mapped into the device address space
+            cudaPointerAttributes a{};
+            if (cudaPointerGetAttributes(&a, h) != cudaSuccess || a.type != cudaMemoryTypeHost ||
+                !a.devicePointer) {
+                cudaGetLastError();
+                return fail(CG_ERR_ARG, "host_ys[%d] is not pinned, device-mapped host memory", i);
+            }
+            h = static_cast<float*>(a.devicePointer);
+        }
+        P->mirror[i] = h;
+        P->plan.gp.layer[i].mirror = h;
+    }
+    ++P->gen;
+    return CG_OK;
+}
+
 int cg_stages_destroy(cg_stages* P) {
+    if (P && P->gexec) cudaGraphExecDestroy(P->gexec);
     delete P;
     return CG_OK;
 }

@@ -51,6 +51,20 @@
 namespace cg {
 namespace {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel, device and
+// size (it costs microseconds of host time; a decode loop launches every step).
+// `done` is the calling launcher's own static (one per kernel instantiation).
+template <typename K>
+cudaError_t set_smem_once(K kern, int smem, int (&done)[64]) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && done[dev] >= smem) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess && dev >= 0 && dev < 64 && smem > done[dev]) done[dev] = smem;
+    return e;
+}
+
+
 constexpr int kChunk = 128;  // K elements per code chunk (8 k16 steps)
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -519,7 +533,8 @@ __global__ void batch_reduce_kernel(const __grid_constant__ BatchParams p) {
 template <int V, int M, int NT, bool SMALL>
 cudaError_t launch_batch_t(const BatchParams& bp, int grid, int smem, cudaStream_t s, bool pdl) {
     auto kern = batch_gemm_kernel<V, M, NT, SMALL>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    static int smem_set[64] = {0};
+    cudaError_t e = set_smem_once(kern, smem, smem_set);
     if (e != cudaSuccess) return e;
     bool reduce = false;
     for (int l = 0; l < bp.n_layers; ++l) reduce |= bp.layer[l].n_slices > 1;

@@ -46,6 +46,8 @@ struct LayerTask {
     int xll;                  // x is the gathered y of a layer pushed earlier in this launch:
                               // read from the LL copy (value, epoch pairs), no stage wait
     int zero_per;             // elements of y each CTA zeroes (rows * n / grid, rounded up to 4)
+    float* mirror;            // host-mapped copy of y written by the kernel once the layer's
+                              // stage is complete (end-to-end path without a D2H copy), or null
 };
 
 // ---- row-shard exchange (cg_comm): every rank owns one device region; a

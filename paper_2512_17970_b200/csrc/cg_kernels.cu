@@ -23,6 +23,20 @@
 namespace cg {
 namespace {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel, device and
+// size (it costs microseconds of host time; a decode loop launches every step).
+// `done` is the calling launcher's own static (one per kernel instantiation).
+template <typename K>
+cudaError_t set_smem_once(K kern, int smem, int (&done)[64]) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && done[dev] >= smem) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess && dev >= 0 && dev < 64 && smem > done[dev]) done[dev] = smem;
+    return e;
+}
+
+
 __device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -958,6 +972,8 @@ struct CtaState {
     float* xc_y[kMaxGroup];       // y
     int xc_elems[kMaxGroup];      // elements of y (rows * n)
     int z_per[kMaxGroup];         // elements of y each CTA zeroes (0: not split)
+    float* mir[kMaxGroup];        // host mirror of y (null: none)
+    unsigned mir_stages;          // stages with a mirrored layer
     // row-shard exchange: counts at launch start, exchanges made, stages that push
     unsigned long long xc_base;
     int xc_n, xc_pushed;
@@ -1571,6 +1587,28 @@ __device__ __noinline__ void xc_push_ll(unsigned char* smem_raw, int off_bar, in
     }
 }
 
+// Host mirror (all threads, after the grid barrier that closed `stage`): this
+// CTA's share of the stage's mirrored layers copied to their host-mapped
+// buffers -- plain stores over PCIe/C2C that overlap the later stages; stream
+// completion makes them visible to the host.
+__device__ __noinline__ void mirror_copy(unsigned char* smem_raw, int off_bar, int stage, int tid,
+                                         int n_layers) {
+    const CtaState& cs = *reinterpret_cast<const CtaState*>(smem_raw + off_bar);
+    for (int l = 0; l < n_layers; ++l) {
+        if (cs.l_stage[l] != stage || !cs.mir[l]) continue;
+        const float* y = cs.xc_y[l];
+        float* h = cs.mir[l];
+        const int elems = cs.xc_elems[l];
+        const int per = (((elems + (int)gridDim.x - 1) / (int)gridDim.x) + 3) & ~3;
+        const int e0 = min((int)blockIdx.x * per, elems), e1 = min(e0 + per, elems);
+        const bool vec = ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(h)) & 15) == 0;
+        const int body = vec ? e0 + ((e1 - e0) & ~3) : e0;
+        for (int e = e0 + 4 * tid; e < body; e += 4 * kThreads)
+            *reinterpret_cast<float4*>(h + e) = __ldcg(reinterpret_cast<const float4*>(y + e));
+        for (int e = body + tid; e < e1; e += kThreads) h[e] = __ldcg(y + e);
+    }
+}
+
 // Grid barrier between dependent stages of a launch (the monotonic counter
 // above).  Everything this CTA wrote in the stage -- plain stores and the bulk
 // (async-proxy) reduce-adds -- is complete and released before the arrival;
@@ -1599,6 +1637,7 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
         ++cs.n_bar;
     }
     __syncthreads();
+    if ((cs.mir_stages >> stage) & 1) mirror_copy(smem_raw, p.off_bar, stage, tid, p.n_layers);
     if (p.xc_local && (p.flags & kFlagXcLL) && !final) {
         // LL: the stage's rows to every rank as (value, epoch) pairs; the next
         // stage's consumers spin on them -- no fence, no wait here
@@ -1699,7 +1738,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             cs.xc_y[l] = L.y;
             cs.xc_elems[l] = (int)(L.rows * p.n);
             cs.z_per[l] = L.n_slices > 1 ? L.zero_per : 0;
+            cs.mir[l] = L.mirror;
         }
+    }
+    if (tid == 0) {
+        unsigned ms = 0;
+        for (int l = 0; l < p.n_layers; ++l)
+            if (p.layer[l].mirror) ms |= 1u << p.layer[l].stage;
+        cs.mir_stages = ms;
     }
     __syncthreads();
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 88] = gtimer();
@@ -1818,6 +1864,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         have = has_next;
     }
     if (zero_todo) zero_arrive(p, tid);  // (a CTA without any task)
+    // the last stage's mirrored outputs are final once every CTA closed its tasks:
+    // one more grid barrier, then the copy (stage_barrier mirrors that stage)
+    if ((cs.mir_stages >> (p.n_stages - 1)) & 1) stage_barrier(p, smem_raw, tid, p.n_stages - 1);
     // the last stage's rows to the peers (its consumers wait in a later
     // launch); the arrival also tells the peers this rank is done reading
     if (p.xc_local) stage_barrier(p, smem_raw, tid, p.n_stages - 1, true);
@@ -1970,7 +2019,8 @@ int grid_for(int64_t total, int threads) {
 template <int V, int M, int U, int KB>
 cudaError_t launch_group_t(const GroupParams& gp, int grid, int smem, bool pdl, cudaStream_t s) {
     auto kern = group_gemv_kernel<V, M, U, KB>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    static int smem_set[64] = {0};
+    cudaError_t e = set_smem_once(kern, smem, smem_set);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid, 1, 1);
@@ -2000,7 +2050,8 @@ template <int V, int M, int U, int KB>
 cudaError_t launch_dump_t(const DumpParams& dp, int64_t n_slices, float* out, int64_t segs,
                           int smem, cudaStream_t s) {
     auto kern = psumbook_dump_kernel<V, M, U, KB>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    static int smem_set[64] = {0};
+    cudaError_t e = set_smem_once(kern, smem, smem_set);
     if (e != cudaSuccess) return e;
     kern<<<dim3((unsigned)n_slices, (unsigned)dp.n), kThreads, smem, s>>>(dp, out, segs);
     return cudaGetLastError();

@@ -403,6 +403,39 @@ class StagedLaunch:
 
         return step
 
+    def bind_host_mirrored(self, x_host, x_dev, y_hosts, stream=None):
+        """End to end with the outputs written to host memory BY THE KERNEL
+        (cg_stages_set_mirror): ``y_hosts[i]`` (pinned CPU tensors, one per layer,
+        or None) receive each layer's y as soon as its stage completes, overlapping
+        the later stages; each call is one H2D of the inputs, the launch, sync --
+        no D2H copy.  Returns a no-argument callable returning ``y_hosts``."""
+        if len(y_hosts) != len(self.layers):
+            raise ShapeError("need one host output (or None) per layer")
+        for y, yd in zip(y_hosts, self.ys):
+            if y is not None and (not y.is_pinned() or y.dtype != yd.dtype
+                                  or tuple(y.shape) != tuple(yd.shape) or not y.is_contiguous()):
+                raise ShapeError("host outputs must be pinned, contiguous and shaped like the "
+                                 "device outputs")
+        k = len(self.layers)
+        ptrs = (ctypes.c_void_p * k)(*[0 if y is None else y.data_ptr() for y in y_hosts])
+        _lib.check(self._lib.cg_stages_set_mirror(self.handle, ptrs))
+        xb = x_host.numel() * x_host.element_size()
+        if x_dev.numel() * x_dev.element_size() < xb:
+            raise ShapeError("device input buffer smaller than the host copy")
+        fn, check = self._lib.cg_stages_run_host, _lib.check
+        args = (self.handle, ctypes.c_void_p(x_host.data_ptr()), ctypes.c_int64(xb),
+                ctypes.c_void_p(x_dev.data_ptr()), None, None, ctypes.c_int64(0),
+                self._stream(stream))
+        keep = (self, x_host, x_dev, list(y_hosts))
+
+        def step():
+            if not keep[0].handle or not keep[0].handle.value:
+                raise ConfigError("the StagedLaunch behind this bound step was closed")
+            check(fn(*args))
+            return keep[3]
+
+        return step
+
     def close(self):
         if getattr(self, "handle", None) is not None and self.handle.value:
             self._lib.cg_stages_destroy(self.handle)

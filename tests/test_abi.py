@@ -20,7 +20,7 @@ HEADER = os.path.join(ROOT, "include", "codegemm_b200.h")
 def declared_functions():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(cg_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(cg_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_declarations_match_binding():
@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
                          text=True, check=True).stdout
-    exported = set(re.findall(r"\bT (cg_[a-z_]+)\b", out))
+    exported = set(re.findall(r"\bT (cg_[a-z0-9_]+)\b", out))
     assert set(declared_functions()) <= exported
 
 

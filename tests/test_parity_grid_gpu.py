@@ -234,3 +234,38 @@ def test_batch_group_launch_matches_single_layers():
     ys = cg.gemm_group(dls, xs)
     for dl, x, y in zip(dls, xs, ys):
         assert np.array_equal(u32(y.cpu().numpy()), u32(dl.gemm(x).cpu().numpy()))
+
+
+def test_staged_launch_host_mirrors():
+    """cg_stages_set_mirror: the kernel writes every layer's output into pinned host
+    memory after its stage (the end-to-end path without a D2H copy) -- the host copies
+    equal the device outputs of the same launch, and the chain matches the oracle."""
+    cfg = cg.QuantConfig(v=4, m=1, b=8, g=128)
+    qs = [cg.random_layer(r, c, cfg, seed=40 + i)
+          for i, (r, c) in enumerate([(2048, 1024), (1024, 2048), (512, 1024)])]
+    layers = [cg.DeviceLayer(q, u=4) for q in qs]
+    x_dev = torch.from_numpy(orc.bench_input_array(1024, 1, 9)).cuda()
+    ys = [torch.empty((q.rows, 1), dtype=torch.float32, device="cuda") for q in qs]
+    plan = cg.StagedLaunch(layers, [x_dev, ys[0], ys[1]], ys, [0, 1, 2])
+    x_host = x_dev.cpu().pin_memory()
+    y_hosts = [torch.full((q.rows, 1), float("nan"), dtype=torch.float32).pin_memory() for q in qs]
+    step = plan.bind_host_mirrored(x_host, x_dev, y_hosts)
+    for _ in range(3):
+        for y in y_hosts:
+            y.fill_(float("nan"))
+        out = step()
+        for yh, yd in zip(out, ys):
+            assert np.array_equal(u32(yh.numpy()), u32(yd.cpu().numpy()))
+    x = x_host.numpy()
+    for q, yh in zip(qs, out):
+        ref = c_oracle.codegemm([p.codes for p in q.planes], [b.entries for b in q.books],
+                                q.scales.scales, x.astype(np.float16), 4, 128)
+        assert_within_tolerance(yh.numpy(), ref, "mirrored chain")
+        x = yh.numpy()
+    with pytest.raises(ValueError):  # pageable host memory is refused
+        _lib_ptrs = (ctypes_c_void_p * 3)(*[torch.empty((q.rows, 1)).data_ptr() for q in qs])
+        cg._lib.check(cg._lib.load().cg_stages_set_mirror(plan.handle, _lib_ptrs))
+
+
+import ctypes as _ct  # noqa: E402
+ctypes_c_void_p = _ct.c_void_p
