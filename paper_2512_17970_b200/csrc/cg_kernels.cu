@@ -973,6 +973,7 @@ struct CtaState {
     int xc_elems[kMaxGroup];      // elements of y (rows * n)
     int z_per[kMaxGroup];         // elements of y each CTA zeroes (0: not split)
     float* mir[kMaxGroup];        // host mirror of y (null: none)
+    long long xc_dl[kMaxRanks];   // peer address deltas (exchange launches)
     unsigned mir_stages;          // stages with a mirrored layer
     // row-shard exchange: counts at launch start, exchanges made, stages that push
     unsigned long long xc_base;
@@ -1514,8 +1515,10 @@ __device__ __noinline__ void xc_prologue(const GroupParams& p, CtaState& cs) {
 // all threads, after the grid barrier that closed `stage`: copy this CTA's
 // share of the stage's pushed layers to every peer, release, signal (at the
 // end of the launch also with nothing to push)
+// (peer address deltas are read from the CTA state in shared memory: a pointer
+// into the kernel parameters read from out-of-line code is a generic load per use)
 __device__ __noinline__ void xc_push(unsigned char* smem_raw, int off_bar, int stage, int tid,
-                                     int n_layers, int world, int rank, const long long* deltas,
+                                     int n_layers, int world, int rank,
                                      const unsigned long long* arrive, bool gpu_scope,
                                      unsigned long long timeout_ns, bool all_stages) {
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + off_bar);
@@ -1532,7 +1535,7 @@ __device__ __noinline__ void xc_push(unsigned char* smem_raw, int off_bar, int s
     }
     for (int r = 0; r < world; ++r) {
         if (r == rank) continue;
-        const long long d = deltas[r];
+        const long long d = cs.xc_dl[r];
         for (int l = 0; l < n_layers; ++l) {
             if ((!all_stages && cs.l_stage[l] != stage) || !((cs.xc_layer_mask >> l) & 1)) continue;
             float* y = cs.xc_y[l];
@@ -1557,7 +1560,7 @@ __device__ __noinline__ void xc_push(unsigned char* smem_raw, int off_bar, int s
 // previous launches (their last exchange), so no LL slot is overwritten while
 // a peer may still read it.
 __device__ __noinline__ void xc_push_ll(unsigned char* smem_raw, int off_bar, int stage, int tid,
-                                        int n_layers, int world, const long long* deltas,
+                                        int n_layers, int world,
                                         const unsigned long long* arrive, unsigned char* ll,
                                         const unsigned char* gbase, unsigned long long timeout_ns) {
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + off_bar);
@@ -1579,9 +1582,10 @@ __device__ __noinline__ void xc_push_ll(unsigned char* smem_raw, int off_bar, in
         for (int e = e0 + tid; e < e1; e += kThreads) {
             const uint32_t v = __float_as_uint(__ldcg(y + e));
             for (int r = 0; r < world; ++r) {
-                float2* d = reinterpret_cast<float2*>(dst0 + deltas[r]) + e;
-                asm volatile("st.volatile.global.v2.u32 [%0], {%1,%2};" ::"l"(d), "r"(v), "r"(epoch)
-                             : "memory");
+                float2* d = reinterpret_cast<float2*>(dst0 + cs.xc_dl[r]) + e;
+                // (no "memory" clobber: the next layer's loads may be issued ahead of
+                // these stores instead of one L2 round trip per layer)
+                asm volatile("st.volatile.global.v2.u32 [%0], {%1,%2};" ::"l"(d), "r"(v), "r"(epoch));
             }
         }
     }
@@ -1642,9 +1646,13 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
         // LL: the stage's rows to every rank as (value, epoch) pairs; the next
         // stage's consumers spin on them -- no fence, no wait here
         if ((cs.xc_push_mask >> stage) & 1) {
-            xc_push_ll(smem_raw, p.off_bar, stage, tid, p.n_layers, p.xc_world, p.xc_delta,
+            unsigned long long* xst = (p.stamps && stage < 4) ? p.stamps + blockIdx.x * 128 + 112 + 2 * stage
+                                                              : nullptr;
+            if (xst && tid == 0) xst[0] = gtimer();
+            xc_push_ll(smem_raw, p.off_bar, stage, tid, p.n_layers, p.xc_world,
                        reinterpret_cast<const unsigned long long*>(p.xc_local + kXcArrive), p.xc_ll,
                        p.xc_gbase, p.xc_timeout_ns);
+            if (xst && tid == 0) xst[1] = gtimer();
         }
         return;
     }
@@ -1654,7 +1662,7 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
         const bool gs = (p.flags & kFlagDbgXcGpuScope) != 0;
         const unsigned long long* arrive =
             reinterpret_cast<const unsigned long long*>(p.xc_local + kXcArrive);
-        xc_push(smem_raw, p.off_bar, stage, tid, p.n_layers, p.xc_world, p.xc_rank, p.xc_delta,
+        xc_push(smem_raw, p.off_bar, stage, tid, p.n_layers, p.xc_world, p.xc_rank,
                 arrive, gs, p.xc_timeout_ns, (p.flags & kFlagXcLL) != 0);
         if (tid == 0) {
             // (the system-scope fence in here is the exchange's main cost: ~1.1 us
@@ -1741,6 +1749,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             cs.mir[l] = L.mirror;
         }
     }
+    if (tid < kMaxRanks) cs.xc_dl[tid] = p.xc_delta[tid];
     if (tid == 0) {
         unsigned ms = 0;
         for (int l = 0; l < p.n_layers; ++l)
