@@ -95,7 +95,12 @@ int list_bytes_for(int64_t rg_per_task, int n) {
 void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms, int reserved) {
     p.fast = false;
     if (p.b > 8 || p.m > 4 || !(p.v == 2 || p.v == 4 || p.v == 8 || p.v == 16)) return;
+    // table / code-stream class: 16 entries + nibbles (b <= 4); 64 entries + 6-bit
+    // stream (b = 5, 6 where instantiated: v = 4, m = 1, u = 4); else 256 + bytes
     p.kbits = p.b <= 4 ? 4 : 8;
+    if ((p.b == 5 || p.b == 6) && (force_u == 0 || force_u == 4) && cg::fused_instantiated(p.v, p.m, 4, 6) &&
+        scale_lg(p, 4) >= 0)
+        p.kbits = 6;
     double best = 1e300;
     const int us[3] = {4, 2, 1};
     for (int ui = 0; ui < 3; ++ui) {
@@ -170,7 +175,7 @@ void plan_fast(cg::Plan& p, int force_u, int force_rg, int sms, int reserved) {
     }
     if (p.fast) {
         // one byte per code, or two per byte for 16-entry tables (b <= 4)
-        p.code_bytes = p.n_slices * p.n_rg * (int64_t)p.m * 16 * p.slice_segs / (p.kbits == 4 ? 2 : 1);
+        p.code_bytes = p.n_slices * p.n_rg * (int64_t)p.m * 16 * p.slice_segs * p.kbits / 8;
         p.scale_bytes = p.n_slices * p.n_rg * (int64_t)p.n_gs * 16 * 2;
     }
 }

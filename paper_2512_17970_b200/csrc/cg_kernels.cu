@@ -102,8 +102,10 @@ __host__ __device__ __forceinline__ int row_mask(int lane) {
 // 0x0f0f0f0f (or shifting it right by 4 first) yields four codes as bytes and
 // the gather's byte extraction is unchanged.  Words are laid out in 16-byte
 // chunks lane-contiguous (u >= 2) or as 8 bytes per lane (u = 1).
-__host__ __device__ __forceinline__ int64_t tile_bytes_of(int u, bool nib) {
-    return nib ? (int64_t)u * 256 : (int64_t)u * 512;
+// cbits: bits per code in the stream -- 4 (16-entry tables), 6 (64-entry
+// tables, u = 4 only: four codes in three bytes, 48 bytes per lane), 8 (else)
+__host__ __device__ __forceinline__ int64_t tile_bytes_of(int u, int cbits) {
+    return cbits == 4 ? (int64_t)u * 256 : (cbits == 6 ? (int64_t)u * 384 : (int64_t)u * 512);
 }
 // byte offset of the lane's 32-bit word wi (nibble mode) inside a tile
 __host__ __device__ __forceinline__ int64_t nib_word_off(int u, int lane, int wi) {
@@ -111,7 +113,7 @@ __host__ __device__ __forceinline__ int64_t nib_word_off(int u, int lane, int wi
 }
 
 __device__ __forceinline__ uint32_t packed_code(const uint8_t* packed, int64_t t, int64_t r,
-                                                int64_t seg, int m, int u, int64_t n_rg, bool nib) {
+                                                int64_t seg, int m, int u, int64_t n_rg, int cbits) {
     const int64_t slice_segs = 32 * u;
     const int64_t slice = seg / slice_segs;
     const int64_t within = seg - slice * slice_segs;
@@ -121,8 +123,14 @@ __device__ __forceinline__ uint32_t packed_code(const uint8_t* packed, int64_t t
     const int64_t rr = r & 15;
     const int64_t slot = rr ^ row_mask((int)lane);
     const int64_t idx = slot * u + uu;  // position in the lane's [slot][u] codes
-    const int64_t tile = ((slice * n_rg + rg) * m + t) * tile_bytes_of(u, nib);
-    if (!nib) return packed[tile + (idx >> 4) * 512 + lane * 16 + (idx & 15)];
+    const int64_t tile = ((slice * n_rg + rg) * m + t) * tile_bytes_of(u, cbits);
+    if (cbits == 8) return packed[tile + (idx >> 4) * 512 + lane * 16 + (idx & 15)];
+    if (cbits == 6) {  // bits [6 idx, 6 idx + 6) of the lane's byte stream (16-byte chunks)
+        const int64_t bit = 6 * idx, p0 = bit >> 3, p1 = p0 + 1;
+        const uint32_t b0 = packed[tile + (p0 >> 4) * 512 + lane * 16 + (p0 & 15)];
+        const uint32_t b1 = p1 < 12 * u ? packed[tile + (p1 >> 4) * 512 + lane * 16 + (p1 & 15)] : 0u;
+        return ((b0 | (b1 << 8)) >> (bit & 7)) & 63u;
+    }
     const uint8_t byte = packed[tile + nib_word_off(u, (int)lane, (int)(idx >> 3)) + (idx & 3)];
     return (idx & 4) ? (byte >> 4) : (byte & 15u);
 }
@@ -133,9 +141,9 @@ __device__ __forceinline__ uint32_t packed_code(const uint8_t* packed, int64_t t
 __global__ void prepack_codes_kernel(const uint16_t* __restrict__ raw, uint8_t* __restrict__ out,
                                      int64_t total, int64_t rows, int64_t segs, int m, int u,
                                      int64_t n_rg, uint32_t code_limit,
-                                     unsigned* __restrict__ bad, int nib) {
+                                     unsigned* __restrict__ bad, int cbits) {
     // one thread per output byte, decoding (slice, rg, t, lane, position)
-    const int64_t tile_bytes = tile_bytes_of(u, nib != 0);
+    const int64_t tile_bytes = tile_bytes_of(u, cbits);
     for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
          o += (int64_t)gridDim.x * blockDim.x) {
         int64_t rest = o;
@@ -147,11 +155,22 @@ __global__ void prepack_codes_kernel(const uint16_t* __restrict__ raw, uint8_t* 
         const int64_t slice = rest / n_rg;
         int64_t lane, idx[2];
         int ncodes;
-        if (!nib) {
+        int sh[2] = {0, 4};
+        if (cbits == 8) {
             const int64_t chunk = in_tile / 512;
             lane = (in_tile % 512) / 16;
             idx[0] = chunk * 16 + (in_tile % 16);
             ncodes = 1;
+        } else if (cbits == 6) {
+            // lane byte p holds bits [8p, 8p + 8) of the lane's 6-bit code stream
+            const int64_t chunk = in_tile / 512;
+            lane = (in_tile % 512) / 16;
+            const int64_t pb = chunk * 16 + (in_tile % 16);
+            idx[0] = (8 * pb) / 6;
+            idx[1] = (8 * pb + 7) / 6;
+            ncodes = idx[1] != idx[0] ? 2 : 1;
+            sh[0] = (int)(6 * idx[0] - 8 * pb);  // may be negative: the code's low bits precede
+            sh[1] = (int)(6 * idx[1] - 8 * pb);
         } else {
             int64_t wi, bw;
             if (u >= 2) {
@@ -170,13 +189,14 @@ __global__ void prepack_codes_kernel(const uint16_t* __restrict__ raw, uint8_t* 
         }
         uint32_t val = 0;
         for (int k = 0; k < ncodes; ++k) {
+            if (idx[k] >= 16 * u) continue;
             const int64_t slot = idx[k] / u, uu = idx[k] % u;
             const int64_t r = rg * 16 + (slot ^ row_mask((int)lane));
             const int64_t seg = slice * 32 * u + lane * u + uu;
             if (r < rows && seg < segs) {
                 const uint16_t c = raw[(t * rows + r) * segs + seg];
                 if (c >= code_limit) atomicOr(bad, 1u);
-                val |= (uint32_t)c << (4 * k);
+                val |= sh[k] >= 0 ? ((uint32_t)c << sh[k]) : ((uint32_t)c >> -sh[k]);
             }
         }
         out[o] = static_cast<uint8_t>(val);
@@ -216,7 +236,7 @@ __global__ void check_codes_kernel(const uint16_t* __restrict__ raw, int64_t tot
 __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed,
                                     const uint16_t* __restrict__ raw16, uint16_t* __restrict__ out,
                                     int64_t rows, int64_t segs, int m, int u, int64_t n_rg,
-                                    int nib) {
+                                    int cbits) {
     const int64_t total = (int64_t)m * rows * segs;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -226,7 +246,7 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed,
             const int64_t seg = i % segs;
             const int64_t r = (i / segs) % rows;
             const int64_t t = i / (segs * rows);
-            out[i] = (uint16_t)packed_code(packed, t, r, seg, m, u, n_rg, nib != 0);
+            out[i] = (uint16_t)packed_code(packed, t, r, seg, m, u, n_rg, cbits);
         }
     }
 }
@@ -293,8 +313,11 @@ struct FusedShape {
     static constexpr int kXFloats = U * 8 * kXQF;
     static constexpr int kPsumBytes = 4 * kPsumFloats;
     static constexpr int kXBytes = 4 * kXFloats;
-    static constexpr bool kNib = KB == 4;  // 16-entry tables: two codes per byte
-    static constexpr int kTileBytes = M * U * (kNib ? 256 : 512);  // codes per (slice, row group)
+    // code stream: KB bits per code (16-entry tables: two codes per byte; 64-entry:
+    // four codes in three bytes, u = 4 only; else one byte)
+    static constexpr bool kNib = KB == 4;
+    static_assert(KB != 6 || U == 4, "6-bit code streams are laid out for u = 4");
+    static constexpr int kTileBytes = M * U * (KB == 4 ? 256 : (KB == 6 ? 384 : 512));
     static constexpr int kLaneBytes = (kNib && U == 1) ? 8 : 16;   // lane offset in a chunk
     static constexpr int kXPerThread = (V * kSliceSegs + kThreads - 1) / kThreads;
     static constexpr int kCPT = kCodes / (4 * kWarps) > 0 ? kCodes / (4 * kWarps) : 1;
@@ -831,7 +854,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ void load_tile(uint4 (&cw)[M][U], const uint8_t* tp) {
     using S = FusedShape<V, M, U, KB>;
-    if constexpr (!S::kNib) {
+    if constexpr (KB == 6) {  // 3 chunks of 16 bytes per lane and codebook: 64 codes x 6 bits
+#pragma unroll
+        for (int t = 0; t < M; ++t)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) cw[t][c] = ldg_stream_v4(tp + (t * 3 + c) * 512);
+    } else if constexpr (!S::kNib) {
 #pragma unroll
         for (int t = 0; t < M; ++t)
 #pragma unroll
@@ -853,14 +881,23 @@ __device__ __forceinline__ void load_tile(uint4 (&cw)[M][U], const uint8_t* tp) 
     }
 }
 
-// the 32-bit word of code idx (bytes = codes), byte mode or nibble mode
-template <bool NIB, int U>
+// the 32-bit word whose byte (idx & 3) is code idx: byte mode, nibble mode, or
+// the 6-bit stream (u = 4: codes 4q..4q+3 = bits [24q, 24q + 24) of the lane's
+// words, spread into bytes with three shifts)
+template <int KB, int U>
 __device__ __forceinline__ uint32_t code_word(const uint4 (&cw)[U], int idx) {
-    if constexpr (!NIB) {
+    if constexpr (KB == 8) {
         return word_of(cw[idx >> 4], (idx >> 2) & 3);
-    } else {
+    } else if constexpr (KB == 4) {
         const uint32_t w = word_of(cw[(idx >> 3) >> 2], (idx >> 3) & 3);
         return (idx & 4) ? ((w >> 4) & 0x0f0f0f0fu) : (w & 0x0f0f0f0fu);
+    } else {
+        const int bit = 24 * (idx >> 2);
+        const int k = bit >> 5, sh = bit & 31;
+        const uint32_t lo = word_of(cw[k >> 2], k & 3);
+        const uint32_t hi = (k + 1 < 12) ? word_of(cw[(k + 1) >> 2], (k + 1) & 3) : 0u;
+        const uint32_t x = __funnelshift_r(lo, hi, sh);
+        return (x & 0x3fu) | ((x << 2) & 0x3f00u) | ((x << 4) & 0x3f0000u) | ((x << 6) & 0x3f000000u);
     }
 }
 
@@ -889,12 +926,12 @@ __device__ __forceinline__ float gather_row_group(const uint4 (&cw)[M][U], const
                 float2 v;
                 {
                     const int idx = i * U + uu;
-                    const uint32_t w = code_word<S::kNib, U>(cw[t], idx);
+                    const uint32_t w = code_word<KB, U>(cw[t], idx);
                     v.x = lds_f32(__byte_perm(w, lb, 0x6504u | ((uint32_t)(idx & 3) << 4)) + region);
                 }
                 {
                     const int idx = (i + 1) * U + uu;
-                    const uint32_t w = code_word<S::kNib, U>(cw[t], idx);
+                    const uint32_t w = code_word<KB, U>(cw[t], idx);
                     v.y = lds_f32(__byte_perm(w, lb, 0x6504u | ((uint32_t)(idx & 3) << 4)) + region);
                 }
                 s2 = (t == 0 && uu == 0) ? v : __fadd2_rn(s2, v);
@@ -1951,7 +1988,7 @@ __global__ void strict_gemm_kernel(const uint8_t* __restrict__ packed,
                                    const uint16_t* __restrict__ x, float* __restrict__ y,
                                    int64_t rows, int64_t segs, int v, int m, int kcount,
                                    int64_t groups, int64_t g_eff, int n, int u, int64_t n_rg,
-                                   int nib) {
+                                   int cbits) {
     pdl_wait();
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= rows * n) return;
@@ -1962,7 +1999,7 @@ __global__ void strict_gemm_kernel(const uint8_t* __restrict__ packed,
         float seg_sum = 0.0f;
         for (int t = 0; t < m; ++t) {
             const uint32_t code = raw16 ? raw16[((int64_t)t * rows + r) * segs + seg]
-                                        : packed_code(packed, t, r, seg, m, u, n_rg, nib != 0);
+                                        : packed_code(packed, t, r, seg, m, u, n_rg, cbits);
             const uint16_t* c = books + ((int64_t)t * kcount + code) * v;
             const uint16_t* xs = x + seg * v * (int64_t)n + col;
             float psum = 0.0f;
@@ -2073,6 +2110,7 @@ bool visit_vmk(int v, int m, int kb, F&& f) {
 #define CG_KB(V_, M_)                                  \
     if (kb == 4) return f.template run<V_, M_, 4>(), true; \
     if (kb == 8) return f.template run<V_, M_, 8>(), true; \
+    if (kb == 6 && V_ == 4 && M_ == 1) return f.template run<V_, M_, 6>(), true; \
     return false;
 #define CG_M(V_)                      \
     if (m == 1) { CG_KB(V_, 1) }      \
@@ -2104,6 +2142,10 @@ struct WithU {
     int u;
     template <int V, int M, int KB>
     void run() {
+        if constexpr (KB == 6) {  // (6-bit streams: u = 4 only -- visit() checks)
+            if constexpr (V == 4 && M == 1) f.template run<V, M, 4, KB>();
+            return;
+        } else {
         if constexpr (M * 4 <= 4) {
             if (u == 4) { f.template run<V, M, 4, KB>(); return; }
         }
@@ -2111,12 +2153,14 @@ struct WithU {
             if (u == 2) { f.template run<V, M, 2, KB>(); return; }
         }
         f.template run<V, M, 1, KB>();
+        }
     }
 };
 
 template <typename F>
 bool visit(int v, int m, int u, int kb, F&& f) {
     if (!(u == 1 || u == 2 || u == 4) || m * u > 4) return false;
+    if (kb == 6 && u != 4) return false;
     WithU<std::remove_reference_t<F>> inner{f, u};
     return visit_vmk(v, m, kb, inner);
 }
@@ -2168,7 +2212,7 @@ cudaError_t launch_prepack_codes(const Plan& p, const uint16_t* raw, uint8_t* pa
                                  unsigned* bad, cudaStream_t s) {
     const int64_t total = p.code_bytes;
     prepack_codes_kernel<<<grid_for(total, 256), 256, 0, s>>>(
-        raw, packed, total, p.rows, p.segs, p.m, p.u, p.n_rg, 1u << p.b, bad, p.kbits == 4);
+        raw, packed, total, p.rows, p.segs, p.m, p.u, p.n_rg, 1u << p.b, bad, p.kbits);
     return cudaGetLastError();
 }
 
@@ -2191,7 +2235,7 @@ cudaError_t launch_unpack_codes(const Plan& p, const uint8_t* packed, const uint
                                 uint16_t* out, cudaStream_t s) {
     const int64_t total = (int64_t)p.m * p.rows * p.segs;
     unpack_codes_kernel<<<grid_for(total, 256), 256, 0, s>>>(packed, raw16, out, p.rows, p.segs,
-                                                            p.m, p.u, p.n_rg, p.kbits == 4);
+                                                            p.m, p.u, p.n_rg, p.kbits);
     return cudaGetLastError();
 }
 
@@ -2216,7 +2260,7 @@ cudaError_t launch_strict_gemm(const Plan& p, const uint8_t* packed, const uint1
     const int64_t blocks = (total + threads - 1) / threads;
     strict_gemm_kernel<<<(unsigned)blocks, threads, 0, s>>>(
         packed, raw16, books, scales, x, y, p.rows, p.segs, p.v, p.m, p.kcount, p.groups,
-        p.g_eff, n, p.u, p.n_rg, p.kbits == 4);
+        p.g_eff, n, p.u, p.n_rg, p.kbits);
     return cudaGetLastError();
 }
 
