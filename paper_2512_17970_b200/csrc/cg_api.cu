@@ -208,6 +208,8 @@ struct cg_layer {
     int rg_cap = 0;          // largest rows-per-task whose task buffers fit shared memory (n=1)
     unsigned long long* stamps = nullptr;  // diagnostics (CG_STAMPS=1)
     int64_t device_bytes = 0;
+    float2* llp = nullptr;          // LL-chain partials (n_slices, rows) of this layer's y
+    int64_t llp_bytes = 0;
     // batch path (K4, n >= 2): its code stream, built on first use, and the
     // split-K partial planes
     bool batch_ok = false;          // config has a batch kernel
@@ -256,6 +258,7 @@ void free_layer(cg_layer* L) {
     cudaFree(L->grid_flags);
     cudaFree(L->rg_cnt);
     cudaFree(L->stamps);
+    cudaFree(L->llp);
     cudaFree(L->bcodes);
     cudaFree(L->bscl);
     cudaFree(L->bws);
@@ -338,7 +341,7 @@ struct StagedPlan {
 
 int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const* ys,
                 const int* stages, int count, int n, const int* x_dtypes, const int* xchg,
-                cg_comm* comm, StagedPlan* out) {
+                cg_comm* comm, StagedPlan* out, bool allow_llc = true) {
     if (count < 1 || count > cg::kMaxGroup)
         return fail(CG_ERR_ARG, "group size %d outside 1..%d", count, cg::kMaxGroup);
     const cg::Plan& p0 = layers[0]->plan;
@@ -509,6 +512,76 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
             for (int i = 0; i < count; ++i) gp.layer[i].dep = -1;
         }
     }
+    // ---- LL chain (single GPU, batch 1, non-deterministic launches; CG_LL_CHAIN=0
+    //      disables): every later-stage x that is an earlier stage's y (same
+    //      pointer and length) is read as the sum of the producer's (value, epoch)
+    //      partials -- the stage barriers, the zeroing and reduce-add of those y
+    //      go away.  Any other alias of an output keeps the barriers.
+    for (int i = 0; i < count; ++i) {
+        gp.layer[i].llx = -1;
+        gp.layer[i].llw = 0;
+        gp.layer[i].llp = nullptr;
+    }
+    {
+        const char* ev = std::getenv("CG_LL_CHAIN");
+        bool llc = allow_llc && !comm && n == 1 && gp.n_stages > 1 &&
+                   !(layers[0]->flags & CG_OPT_DETERMINISTIC) && !(gp.flags & cg::kFlagRowDeps) &&
+                   !(ev && std::atoi(ev) == 0);
+        int nprod = 0;
+        for (int i = 0; llc && i < count; ++i) {
+            cg::LayerTask& t = gp.layer[i];
+            int src = -1;
+            for (int j = 0; t.x32 && j < count; ++j)
+                if (gp.layer[j].y == t.x32 && gp.layer[j].stage < t.stage && gp.layer[j].rows == t.cols)
+                    src = j;
+            if (src < 0) {  // an x that is not an earlier stage's whole y must not touch any y
+                const uintptr_t xa = t.x32 ? reinterpret_cast<uintptr_t>(t.x32)
+                                           : reinterpret_cast<uintptr_t>(t.x);
+                const uintptr_t xb = xa + (uintptr_t)(t.cols * (t.x32 ? 4 : 2));
+                for (int j = 0; j < count; ++j) {
+                    const uintptr_t ya = reinterpret_cast<uintptr_t>(gp.layer[j].y);
+                    if (xa < ya + (uintptr_t)(gp.layer[j].rows * 4) && ya < xb) llc = false;
+                }
+                continue;
+            }
+            t.llx = src;
+            ++nprod;
+        }
+        // a producer's partial planes and epoch live in its cg_layer: one use per launch
+        for (int i = 0; llc && i < count; ++i)
+            for (int j = 0; j < count; ++j)
+                if (j != i && gp.layer[j].llx >= 0 && layers[i] == layers[gp.layer[j].llx] &&
+                    i != gp.layer[j].llx)
+                    llc = false;
+        if (llc && nprod > 0) {
+            for (int i = 0; i < count; ++i) {
+                cg::LayerTask& t = gp.layer[i];
+                if (t.llx < 0) continue;
+                cg::LayerTask& P = gp.layer[t.llx];
+                cg_layer* PL = layers[t.llx];
+                if (!P.llp) {
+                    // the producer's partial planes, zero-filled once (epoch 0 never matches)
+                    const int64_t bytes = PL->plan.n_slices * PL->plan.rows * 8;
+                    if (bytes > PL->llp_bytes) {
+                        cudaFree(PL->llp);
+                        PL->device_bytes -= PL->llp_bytes;
+                        PL->llp = nullptr;
+                        PL->llp_bytes = 0;
+                        int rc = dev_alloc(PL, &PL->llp, (size_t)bytes, "LL-chain partials alloc");
+                        if (rc) return rc;
+                        cudaMemset(PL->llp, 0, (size_t)bytes);
+                        PL->llp_bytes = bytes;
+                    }
+                    P.llp = PL->llp;
+                    P.rg_cnt = PL->rg_cnt;  // its launch generation: the epoch
+                    t.llw = 1;              // the first consumer writes the reduced y
+                }
+            }
+            gp.flags |= cg::kFlagLLChain;
+        } else {
+            for (int i = 0; i < count; ++i) gp.layer[i].llx = -1;
+        }
+    }
     // ---- per-stage task split.  A layer's plan fills the GPU on its own
     //      (~1 task per SM); a stage of several layers would then run several
     //      tasks -- several Psumbook builds -- per CTA.  Re-split the rows of
@@ -578,7 +651,8 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
         const int64_t elems = gp.layer[i].rows * n;
         if (elems >= (int64_t(1) << 31))
             return fail(CG_ERR_SHAPE, "layer %d: rows * n = %lld exceeds 2^31", i, (long long)elems);
-        gp.layer[i].zero_per = (int)((((elems + grid - 1) / grid) + 3) & ~int64_t(3));
+        gp.layer[i].zero_per =
+            gp.layer[i].llp ? 0 : (int)((((elems + grid - 1) / grid) + 3) & ~int64_t(3));
     }
     // fix-up list / owned-ticket targets (deterministic) or the staging buffer
     // of a task's partial rows (reduce-add): the larger of the two
@@ -1153,6 +1227,7 @@ int cg_gemm_stages_xchg(cg_layer* const* layers, const void* const* xs, const in
 struct cg_stages {
     StagedPlan plan;
     float* mirror[cg::kMaxGroup] = {nullptr};  // host-mapped y copies (cg_stages_set_mirror)
+    bool no_llc = false;  // mirrors copy y at stage barriers: plan without the LL chain
     int gen = 0;  // bumped whenever the launch parameters change
     // cg_stages_run_host replays one CUDA graph (H2D, the launch, D2H): a direct
     // cooperative launch costs tens of microseconds of host time per call
@@ -1173,12 +1248,12 @@ struct cg_stages {
 };
 
 namespace {
-int replan_if_needed(cg_stages* P) {
-    bool stale = false;
+int replan_if_needed(cg_stages* P, bool force = false) {
+    bool stale = force;
     for (int i = 0; i < P->count; ++i) stale |= P->layers[i]->ws != P->ws[i];
     if (!stale) return CG_OK;  // (a layer's workspace grew for a wider call since)
     int rc = plan_stages(P->layers, P->xs, P->ys, P->stages, P->count, P->n, P->x_dtypes,
-                         P->comm ? P->xchg : nullptr, P->comm, &P->plan);
+                         P->comm ? P->xchg : nullptr, P->comm, &P->plan, !P->no_llc);
     if (rc) return rc;
     for (int i = 0; i < P->count; ++i) P->ws[i] = P->layers[i]->ws;
     for (int i = 0; i < P->count; ++i) P->plan.gp.layer[i].mirror = P->mirror[i];
@@ -1316,6 +1391,13 @@ int cg_stages_set_mirror(cg_stages* P, void* const* host_ys) {
         }
         P->mirror[i] = h;
         P->plan.gp.layer[i].mirror = h;
+    }
+    bool any = false;
+    for (int i = 0; i < P->count; ++i) any |= P->mirror[i] != nullptr;
+    if (any != P->no_llc) {
+        P->no_llc = any;
+        int rc = replan_if_needed(P, true);
+        if (rc) return rc;
     }
     ++P->gen;
     return CG_OK;

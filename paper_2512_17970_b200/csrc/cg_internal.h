@@ -43,6 +43,14 @@ struct LayerTask {
     unsigned long long* rg_cnt;  // [0] launches completed, [1 + rg] row-group completions
                                  // (this layer is a producer for a later layer), or null
     int xchg;                 // kXchgPush | kXchgWait (row-shard exchange launches), else 0
+    // LL chain (kFlagLLChain, single GPU): a producer layer (y read by a later stage
+    // of the launch) writes its split-K partial rows as (value, epoch) pairs into
+    // llp[slice][row] instead of reducing them into y; a consumer (llx = producer)
+    // sums the partials of its x slice in slice order, spinning on the epoch -- no
+    // grid barrier, no y zeroing, deterministic; the consumer with llw set writes
+    // the reduced y (its tasks of row block 0)
+    float2* llp;
+    int llx, llw;
     int xll;                  // x is the gathered y of a layer pushed earlier in this launch:
                               // read from the LL copy (value, epoch pairs), no stage wait
     int zero_per;             // elements of y each CTA zeroes (rows * n / grid, rounded up to 4)
@@ -114,6 +122,7 @@ constexpr int kFlagLastArriver = 4;  // a layer has more tasks than the grid: la
 constexpr int kFlagDeterministic = 16;  // split-K by tickets + ordered sums (else L2 reduce-add)
 constexpr int kFlagXRegs = 32;  // x staged through registers (unaligned x / odd cols / n > 1)
 constexpr int kFlagXcLL = 128;  // exchange launch: LL stage pushes (GroupParams::xc_ll)
+constexpr int kFlagLLChain = 1 << 16;  // staged launch: LL partials between stages, no barriers
 // diagnostics only (CG_DEBUG_FLAGS): wrong results, phase isolation for timing
 constexpr int kFlagRowDeps = 64;  // stages ordered by row-group readiness, not grid barriers
 constexpr int kFlagDirectAdd = 1 << 14;  // split-K partials red.add'ed into y even at n == 1

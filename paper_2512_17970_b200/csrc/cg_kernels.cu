@@ -415,6 +415,57 @@ __device__ __forceinline__ void load_x_ll(uint16_t (&r)[FusedShape<V, M, U, KB>:
     }
 }
 
+// x of an LL-chain consumer: element e = sum over the producer's slices (in slice
+// order: deterministic) of its partial row e, each an (value, epoch) pair spun on
+// until this launch's epoch shows; the writer consumer also stores the reduced y
+__device__ __forceinline__ float llc_sum(const float2* llp, int64_t rows, int ns, int64_t e,
+                                         unsigned epoch) {
+    float acc = 0.0f;
+    for (int s0 = 0; s0 < ns; s0 += 8) {
+        uint32_t v[8], ep[8];
+        const int k = min(8, ns - s0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)  // up to 8 partials in flight
+            if (j < k)
+                asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];"
+                             : "=r"(v[j]), "=r"(ep[j]) : "l"(llp + (int64_t)(s0 + j) * rows + e));
+        unsigned long long t0 = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j >= k) break;
+            while (ep[j] != epoch) {
+                asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];"
+                             : "=r"(v[j]), "=r"(ep[j]) : "l"(llp + (int64_t)(s0 + j) * rows + e));
+                const unsigned long long t = gtimer();
+                if (t0 == 0) t0 = t;
+                else if (t - t0 > 2000000000ull) __trap();  // a producer never wrote (2 s)
+            }
+            acc += __uint_as_float(v[j]);
+        }
+    }
+    return acc;
+}
+
+template <int V, int M, int U, int KB>
+__device__ __forceinline__ void load_x_llc(uint16_t (&r)[FusedShape<V, M, U, KB>::kXPerThread],
+                                           const LayerTask& L, const LayerTask& P, unsigned epoch,
+                                           bool write_y, int64_t slice, int tid) {
+    using S = FusedShape<V, M, U, KB>;
+    const int64_t e0 = slice * (int64_t)(S::kSliceSegs * V);
+#pragma unroll
+    for (int i = 0; i < S::kXPerThread; ++i) {
+        const int l = tid + i * kThreads;
+        const int64_t e = e0 + l;
+        uint16_t h = 0;
+        if (l < S::kSliceSegs * V && e < L.cols) {
+            const float y = llc_sum(P.llp, P.rows, (int)P.n_slices, e, epoch);
+            if (write_y) P.y[e] = y;
+            h = __half_as_ushort(__float2half_rn(y));
+        }
+        r[i] = h;
+    }
+}
+
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ void store_x(float* xs,
                                         const uint16_t (&r)[FusedShape<V, M, U, KB>::kXPerThread],
@@ -1217,7 +1268,8 @@ __device__ __forceinline__ bool next_task_s(const CtaState& cs, int nl, int ns, 
 // unaligned slices; not for a row-readiness consumer (its x is waited for
 // per row group inside the task, after the copy would have been issued)
 __device__ __forceinline__ bool x_by_copy(const GroupParams& p, const LayerTask& L) {
-    return p.n == 1 && !(p.flags & kFlagXRegs) && (L.x32 == nullptr || L.dep < 0) && !L.xll;
+    return p.n == 1 && !(p.flags & kFlagXRegs) && (L.x32 == nullptr || L.dep < 0) && !L.xll &&
+           L.llx < 0;
 }
 
 // Task geometry (all task counts fit in 32 bits).
@@ -1329,7 +1381,10 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
         __syncthreads();
     }
     uint16_t xreg[S::kXPerThread];
-    if (L.xll) load_x_ll<V, M, U, KB>(xreg, L, p, (unsigned)(cs.xc_base + 1), slice, n, 0, tid);
+    if (L.llx >= 0)
+        load_x_llc<V, M, U, KB>(xreg, L, p.layer[L.llx], (unsigned)(cs.l_gen[L.llx] + 1),
+                                L.llw && g.rb == 0, slice, tid);
+    else if (L.xll) load_x_ll<V, M, U, KB>(xreg, L, p, (unsigned)(cs.xc_base + 1), slice, n, 0, tid);
     else if (!x_by_copy(p, L)) load_x<V, M, U, KB>(xreg, L, slice, n, 0, tid);
 
     // 2. the previous task is done with the table; the staging buffer of two
@@ -1359,7 +1414,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     // red.global.add (staging would shrink tasks by the column count)
     const bool direct = split && !(p.flags & kFlagDeterministic) &&
                         (n > 1 || (p.flags & kFlagDirectAdd));
-    const bool stage_out = split && !(p.flags & kFlagDeterministic) && !direct;
+    const bool stage_out = (split && !(p.flags & kFlagDeterministic) && !direct) || L.llp != nullptr;
     const int64_t row_step = (int64_t)kWarps * 16;
 
     for (int col = 0; col < n; ++col) {
@@ -1444,7 +1499,18 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
         }
     }
     CG_STAMP(1)
-    if (stage_out) {
+    if (L.llp) {
+        // LL-chain producer: the task's partial rows (slice `slice`) as (value,
+        // epoch) pairs -- no reduction, no zeroed y, no barrier for the consumers
+        __syncthreads();
+        const float* stg = reinterpret_cast<const float*>(smem_raw + p.off_stage[buf]);
+        const uint32_t epoch = (uint32_t)(cs.l_gen[l] + 1);
+        const int64_t r1 = min(rg1 * 16, L.rows);
+        float2* dst = L.llp + (int64_t)slice * L.rows + rg0 * 16;
+        for (int64_t e = tid; e < r1 - rg0 * 16; e += kThreads)
+            asm volatile("st.volatile.global.v2.u32 [%0], {%1,%2};" ::"l"(dst + e),
+                         "r"(__float_as_uint(stg[e])), "r"(epoch));
+    } else if (stage_out) {
         // flush the task's partial rows into y (L2 reduce-add); y was zeroed
         // by the grid at kernel start -- wait for that (arrival 1) once
         __syncthreads();
@@ -1467,7 +1533,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     }
     __syncthreads();
     if (tid == 0) {
-        if (L.rg_cnt) {  // a later stage reads this y: signal at the next task start
+        if (L.rg_cnt && !L.llp) {  // a later stage reads this y: signal at the next task start
             cs.sig_layer = l;
             cs.sig_rg0 = rg0;
             cs.sig_rg1 = rg1;
@@ -1828,7 +1894,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0 && have && cs.l_stage[c.l] == 0)
         issue_inputs<V, M, U, KB>(p, c, 0, smem_raw, false, true);
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 92] = gtimer();
-    if (p.flags & kFlagRowDeps) {  // producer generations (row deps), one layer per warp
+    if (p.flags & (kFlagRowDeps | kFlagLLChain)) {  // producer generations, one layer per warp
         for (int l = tid >> 5; l < p.n_layers; l += kWarps) {
             if ((tid & 31) == 0 && p.layer[l].rg_cnt) {
                 unsigned long long gv;
@@ -1864,7 +1930,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // the arrival (fenced) is made after the CTA's first Psumbook build,
         // when these stores have long completed -- off the prologue's path
-        if ((any || (p.flags & kFlagRowDeps)) && tid == 0) {
+        if ((any || (p.flags & (kFlagRowDeps | kFlagLLChain))) && tid == 0) {
             cs.n_arrive = 1;
             cs.zero_pending = 1;
         }
@@ -1882,7 +1948,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 zero_arrive(p, tid);
                 zero_todo = false;
             }
-            if (!(p.flags & kFlagRowDeps)) stage_barrier(p, smem_raw, tid, stage);
+            if (!(p.flags & (kFlagRowDeps | kFlagLLChain))) stage_barrier(p, smem_raw, tid, stage);
             ++stage;
             if (tid == 0 && have && stage == target)
                 issue_inputs<V, M, U, KB>(p, c, buf, smem_raw, false, true);
@@ -1922,7 +1988,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0) {
         bulk_wait_all();
         signal_rows(p, cs);
-        if ((p.flags & kFlagRowDeps) && blockIdx.x == 0) {
+        if ((p.flags & (kFlagRowDeps | kFlagLLChain)) && blockIdx.x == 0) {
             // every CTA read the generations before its arrival 1
             grid_wait(p, cs, 1);
             for (int l = 0; l < p.n_layers; ++l)
