@@ -513,10 +513,13 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
         }
     }
     // ---- LL chain (single GPU, batch 1, non-deterministic launches; CG_LL_CHAIN=0
-    //      disables): every later-stage x that is an earlier stage's y (same
-    //      pointer and length) is read as the sum of the producer's (value, epoch)
-    //      partials -- the stage barriers, the zeroing and reduce-add of those y
-    //      go away.  Any other alias of an output keeps the barriers.
+    //      disables): a later-stage x that is an earlier stage's y (same pointer
+    //      and length), produced in at most CG_LL_MAX_SLICES (8) K-slices, is read
+    //      as the sum of the producer's (value, epoch) partials -- the zeroing and
+    //      reduce-add of that y go away, and so does the grid barrier before the
+    //      consumer's stage when all its aliased inputs come this way.  (Wider
+    //      producers cost the consumer more spinning loads than a barrier.)  Any
+    //      other alias of an output keeps the barriers.
     for (int i = 0; i < count; ++i) {
         gp.layer[i].llx = -1;
         gp.layer[i].llw = 0;
@@ -524,6 +527,8 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
     }
     {
         const char* ev = std::getenv("CG_LL_CHAIN");
+        const char* em = std::getenv("CG_LL_MAX_SLICES");
+        const int64_t max_slices = em ? std::atoi(em) : 8;
         bool llc = allow_llc && !comm && n == 1 && gp.n_stages > 1 &&
                    !(layers[0]->flags & CG_OPT_DETERMINISTIC) && !(gp.flags & cg::kFlagRowDeps) &&
                    !(ev && std::atoi(ev) == 0);
@@ -534,6 +539,8 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
             for (int j = 0; t.x32 && j < count; ++j)
                 if (gp.layer[j].y == t.x32 && gp.layer[j].stage < t.stage && gp.layer[j].rows == t.cols)
                     src = j;
+            if (src >= 0 && gp.layer[src].n_slices > max_slices) src = -2;  // barrier path
+            if (src == -2) continue;
             if (src < 0) {  // an x that is not an earlier stage's whole y must not touch any y
                 const uintptr_t xa = t.x32 ? reinterpret_cast<uintptr_t>(t.x32)
                                            : reinterpret_cast<uintptr_t>(t.x);
@@ -578,6 +585,20 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
                 }
             }
             gp.flags |= cg::kFlagLLChain;
+            // the barrier before stage t stays if a stage-t layer reads an earlier
+            // stage's y the ordinary way (every alias is a whole earlier y here)
+            unsigned skip = 0;
+            for (int st = 0; st + 1 < gp.n_stages; ++st) {
+                bool need = false;
+                for (int i = 0; i < count; ++i) {
+                    const cg::LayerTask& t = gp.layer[i];
+                    if (t.stage != st + 1 || t.llx >= 0 || !t.x32) continue;
+                    for (int j = 0; j < count; ++j)
+                        if (gp.layer[j].y == t.x32 && gp.layer[j].stage <= st) need = true;
+                }
+                if (!need) skip |= 1u << st;
+            }
+            gp.bar_skip = skip;
         } else {
             for (int i = 0; i < count; ++i) gp.layer[i].llx = -1;
         }

@@ -83,6 +83,7 @@ struct GroupParams {
     int n_stages;             // stage s+1 starts after every CTA finished stage s
     int n;                    // batch columns
     int flags, pf_dist;
+    unsigned bar_skip;  // LL chain: bit s set = no grid barrier after stage s
     // dynamic shared-memory layout (bytes from the dynamic smem start); the
     // Psumbook sits at a 64 KB-aligned shared-window address (see cg_api.cu)
     int off_psum, off_books, off_x, off_bar, off_list, list_cap;

@@ -1948,7 +1948,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 zero_arrive(p, tid);
                 zero_todo = false;
             }
-            if (!(p.flags & (kFlagRowDeps | kFlagLLChain))) stage_barrier(p, smem_raw, tid, stage);
+            if (!(p.flags & kFlagRowDeps) && !((p.bar_skip >> stage) & 1u))
+                stage_barrier(p, smem_raw, tid, stage);
             ++stage;
             if (tid == 0 && have && stage == target)
                 issue_inputs<V, M, U, KB>(p, c, buf, smem_raw, false, true);
