@@ -424,24 +424,35 @@ __device__ __forceinline__ float llc_sum(const float2* llp, int64_t rows, int ns
     for (int s0 = 0; s0 < ns; s0 += 8) {
         uint32_t v[8], ep[8];
         const int k = min(8, ns - s0);
+        const float2* a = llp + (int64_t)s0 * rows + e;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)  // up to 8 partials in flight
+        for (int j = 0; j < 8; ++j) {  // up to 8 partials in flight
+            ep[j] = epoch;
             if (j < k)
                 asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];"
-                             : "=r"(v[j]), "=r"(ep[j]) : "l"(llp + (int64_t)(s0 + j) * rows + e));
-        unsigned long long t0 = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (j >= k) break;
-            while (ep[j] != epoch) {
-                asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];"
-                             : "=r"(v[j]), "=r"(ep[j]) : "l"(llp + (int64_t)(s0 + j) * rows + e));
-                const unsigned long long t = gtimer();
-                if (t0 == 0) t0 = t;
-                else if (t - t0 > 2000000000ull) __trap();  // a producer never wrote (2 s)
-            }
-            acc += __uint_as_float(v[j]);
+                             : "=r"(v[j]), "=r"(ep[j]) : "l"(a + j * rows));
         }
+        // poll in rounds: every partial still stale is re-read in the same round
+        // (one round trip per round, not one per partial)
+        unsigned long long t0 = 0;
+        while (true) {
+            bool ready = true;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ready &= ep[j] == epoch;
+            if (ready) break;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (ep[j] != epoch)
+                    asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];"
+                                 : "=r"(v[j]), "=r"(ep[j]) : "l"(a + j * rows));
+            const unsigned long long t = gtimer();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 2000000000ull) __trap();  // a producer never wrote (2 s)
+            __nanosleep(64);  // (fewer polls in flight: less L2 queueing; 8B block -0.2 us)
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (j < k) acc += __uint_as_float(v[j]);
     }
     return acc;
 }
@@ -885,6 +896,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// fine-grained diagnostics of one task switch (CG_FINE_STAMPS builds only)
+#ifdef CG_FINE_STAMPS
+#define CG_FST(k) \
+    if (p.stamps && tid == 0 && task_idx == 1) p.stamps[blockIdx.x * 128 + 112 + (k)] = gtimer();
+#else
+#define CG_FST(k)
+#endif
+
 // ---------------------------------------------------------------------------
 // K2: fused Psumbook build + code-gather accumulate (persistent, task-driven)
 //
@@ -1054,6 +1073,7 @@ struct CtaState {
     // this CTA's task list, enumerated once at kernel start (task switches
     // must not walk the layer table: indexed parameter loads are slow)
     int l_stage[kMaxGroup], l_tasks[kMaxGroup];  // per layer, copied from the parameters
+    int l_xcopy[kMaxGroup];       // per layer: x travels by bulk copy (x_by_copy)
     unsigned long long l_gen[kMaxGroup];  // producer layers: completed launches (row deps)
     // per layer, copied at kernel start by one thread each (loops over the layer
     // table would be chains of dependent indexed parameter loads, ~0.2 us per layer)
@@ -1368,6 +1388,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
 #pragma unroll
     for (int d = 0; d < D; ++d)
         if (d < my_rgs) load_tile<V, M, U, KB>(tb[d], cptr + d * kStep);
+    CG_FST(3)
     if (tid == 0) signal_rows(p, cs);  // the previous task, if a producer
     if (L.dep >= 0) {
         // x is an earlier stage's y: wait for the row groups this slice reads
@@ -1386,6 +1407,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
                                 L.llw && g.rb == 0, slice, tid);
     else if (L.xll) load_x_ll<V, M, U, KB>(xreg, L, p, (unsigned)(cs.xc_base + 1), slice, n, 0, tid);
     else if (!x_by_copy(p, L)) load_x<V, M, U, KB>(xreg, L, slice, n, 0, tid);
+    CG_FST(4)
 
     // 2. the previous task is done with the table; the staging buffer of two
     //    tasks ago has been read by its flush; the next task's inputs start
@@ -1439,6 +1461,9 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
         if (!(p.flags & kFlagDbgSkipBuild))
             build_psumbook_smem<V, M, U, KB>(psum, raw, xs,
                                              L.kcount, tid);
+#ifdef CG_FINE_STAMPS
+        if (p.stamps && lane == 0 && task_idx == 1) p.stamps[blockIdx.x * 128 + 96 + warp] = gtimer();
+#endif
         __syncthreads();
         if (col == 0) CG_STAMP(6)
         if (col == 0 && first_task) pdl_launch_dependents();
@@ -1728,7 +1753,11 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
     close_task(p, smem_raw, tid);  // deterministic split-K: pending ordered sums
     CtaState& cs = *reinterpret_cast<CtaState*>(smem_raw + p.off_bar);
     unsigned long long* st =
+#ifdef CG_FINE_STAMPS
+        nullptr;  // (slots 96.. hold per-warp stamps)
+#else
         (p.stamps && cs.n_bar < 7) ? p.stamps + blockIdx.x * 128 + 96 + 4 * cs.n_bar : nullptr;
+#endif
     if (tid == 0) {
         if (st) st[0] = gtimer();
         cs.prev_layer = -1;
@@ -1850,6 +1879,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             cs.xc_elems[l] = (int)(L.rows * p.n);
             cs.z_per[l] = L.n_slices > 1 ? L.zero_per : 0;
             cs.mir[l] = L.mirror;
+            cs.l_xcopy[l] = x_by_copy(p, L) ? 1 : 0;
         }
     }
     if (tid < kMaxRanks) cs.xc_dl[tid] = p.xc_delta[tid];
@@ -1942,6 +1972,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int buf = 0, task_idx = 0;
     bool first = true;
     while (true) {
+        CG_FST(0)
         const int target = have ? cs.l_stage[c.l] : p.n_stages - 1;
         while (stage < target) {  // (CTAs without tasks in a stage still take part)
             if (zero_todo) {  // the zeroing arrival precedes every stage arrival
@@ -1951,9 +1982,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!(p.flags & kFlagRowDeps) && !((p.bar_skip >> stage) & 1u))
                 stage_barrier(p, smem_raw, tid, stage);
             ++stage;
-            if (tid == 0 && have && stage == target)
+            if (tid == 0 && have && stage == target && cs.l_xcopy[c.l])
                 issue_inputs<V, M, U, KB>(p, c, buf, smem_raw, false, true);
         }
+        CG_FST(1)
         if (!have) break;
         TaskCoord nc = c;
         bool has_next;
@@ -1968,6 +2000,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             has_next = next_task_s(cs, p.n_layers, p.n_stages, nc);  // beyond the list (rare)
         }
         const bool x_next = has_next && cs.l_stage[nc.l] == stage;
+        CG_FST(2)
         run_task<V, M, U, KB>(p, c, buf, first, has_next, x_next, nc, smem_raw, tid, task_idx++,
                               zero_todo);
         zero_todo = false;

@@ -102,3 +102,12 @@ for b in range(4):
     show(f"xchg{b} pushed", st[:, 112 + 2 * b])
     show(f"xchg{b} all arrived", st[:, 113 + 2 * b])
 show("kernel end", st[:, 127])
+if os.environ.get("GRAN"):  # timer granularity: gcd of the stamp offsets
+    v = st[st > 0] - t0
+    print("stamp granularity (ns):", int(np.gcd.reduce(v[v > 0].astype(np.int64))),
+          "sample offsets:", sorted(set((v % 1000).tolist()))[:12])
+if os.environ.get("FINE"):
+    for w in range(16):
+        show(f"task1 warp{w:2d} at post-build barrier", st[:, 96 + w])
+    for k, nm in enumerate(("loop top", "stages passed", "before run_task", "tiles issued", "x loaded")):
+        show(f"task1 fine {nm}", st[:, 112 + k])
