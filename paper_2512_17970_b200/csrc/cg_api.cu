@@ -84,7 +84,8 @@ int raw_input_bytes(const cg::Plan& p, int u, int x_elem_bytes = 2) {
 }
 // fix-up list entries (deterministic) or the split-K staging rows (reduce-add)
 int list_bytes_for(int64_t rg_per_task, int n) {
-    return (int)std::max<int64_t>(std::max((rg_per_task * n + 16) * 16, rg_per_task * 16 * n * 4), 256);
+    // (>= 512: the kernel prologue lists the CTA's tasks through 128 ints of it)
+    return (int)std::max<int64_t>(std::max((rg_per_task * n + 16) * 16, rg_per_task * 16 * n * 4), 512);
 }
 
 // Planner: pick u (segments per lane) and rows per task for the fused kernel.
@@ -613,6 +614,9 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
     // (a comm launch runs the comm's grid on every rank: its barrier flags and
     // exchange counters count arrivals of exactly that many CTAs)
     const int sms = comm ? comm->ctas : layers[0]->sms;
+    // contiguous per-CTA task ranges with Psumbook reuse (reduce-add split-K, one column)
+    const bool contig = !(layers[0]->flags & CG_OPT_DETERMINISTIC) && n == 1 &&
+                        std::getenv("CG_NO_CONTIG") == nullptr;
     {
         bool forced = false;
         // columns the per-task smem buffers scale with: reduce-add mode adds the
@@ -629,19 +633,73 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
                 for (int i = 0; i < count; ++i)
                     if (gp.layer[i].stage == st) max_rg = std::max(max_rg, gp.layer[i].n_rg);
                 const double f_rg = 2.0 / (0.019 * p0.u * p0.m);  // ~2 us of fixed cost per task
-                double best = 1e300;
-                int64_t best_rg = 0;
-                for (int64_t rg = 1; rg <= max_rg; ++rg) {
-                    if (rg > cap) break;
+                auto stage_tasks = [&](int64_t rg) {
                     int64_t tasks = 0;
                     for (int i = 0; i < count; ++i)
                         if (gp.layer[i].stage == st)
                             tasks += gp.layer[i].n_slices * ((gp.layer[i].n_rg + rg - 1) / rg);
+                    return tasks;
+                };
+                double best = 1e300;
+                int64_t best_rg = 0;
+                for (int64_t rg = 1; rg <= max_rg; ++rg) {
+                    if (rg > cap) break;
+                    const int64_t tasks = stage_tasks(rg);
                     const double waves = (double)((tasks + sms - 1) / sms);
                     const double cost = waves * (f_rg + (double)rg) + 1e-6 * (double)rg;
                     if (cost < best) {
                         best = cost;
                         best_rg = rg;
+                    }
+                }
+                if (contig && best_rg > 0) {
+                    // contiguous task ranges: a CTA rebuilds the Psumbook only when its
+                    // range enters another (layer, K-slice); a task that reuses the table
+                    // costs ~1/2 of the fixed cost (input wait, flush).  Candidates: the
+                    // smallest rg that fits the stage in k tasks per CTA, k = 1..24; cost
+                    // = the slowest CTA's rows + per-task and per-build costs.
+                    auto contig_cost = [&](int64_t rg) {
+                        const int64_t T = stage_tasks(rg);
+                        if (T <= sms) return f_rg + (double)rg;
+                        double worst = 0.0;
+                        for (int64_t c = 0; c < sms; ++c) {
+                            const int64_t lo = c * T / sms, hi = (c + 1) * T / sms;
+                            if (hi <= lo) continue;
+                            // (layer, slice) column of stage task g: columns numbered in order
+                            auto column = [&](int64_t g) {
+                                int64_t col0 = 0;
+                                for (int i = 0; i < count; ++i) {
+                                    const cg::LayerTask& t = gp.layer[i];
+                                    if (t.stage != st) continue;
+                                    const int64_t nrb = (t.n_rg + rg - 1) / rg;
+                                    const int64_t nt = t.n_slices * nrb;
+                                    if (g < nt) return col0 + g / nrb;
+                                    g -= nt;
+                                    col0 += t.n_slices;
+                                }
+                                return col0;
+                            };
+                            const double builds = (double)(column(hi - 1) - column(lo) + 1);
+                            const double cost =
+                                (double)(hi - lo) * ((double)rg + 0.5 * f_rg) + 0.5 * f_rg * builds;
+                            worst = std::max(worst, cost);
+                        }
+                        return worst;
+                    };
+                    double cbest = contig_cost(best_rg);
+                    for (int64_t k = 1; k <= 24; ++k) {
+                        int64_t lo = 1, hi = std::min<int64_t>(max_rg, cap);
+                        if (stage_tasks(hi) > k * sms) continue;
+                        while (lo < hi) {  // smallest rg with at most k tasks per CTA
+                            const int64_t mid = (lo + hi) / 2;
+                            if (stage_tasks(mid) <= k * sms) hi = mid;
+                            else lo = mid + 1;
+                        }
+                        const double cst = contig_cost(lo);
+                        if (cst < cbest) {
+                            cbest = cst;
+                            best_rg = lo;
+                        }
                     }
                 }
                 if (best_rg < 1) continue;
@@ -706,6 +764,7 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
     // cooperative attribute (it may serialise their grids); each grid fits
     if (comm && comm->ctas < layers[0]->sms) gp.flags |= cg::kFlagDbgNoCoop;
     if (layers[0]->flags & CG_OPT_DETERMINISTIC) gp.flags |= cg::kFlagDeterministic;
+    if (contig) gp.flags |= cg::kFlagContig;
     if (const char* e = std::getenv("CG_DEBUG_FLAGS")) gp.flags |= std::atoi(e);
     out->gp = gp;
     out->grid = grid;

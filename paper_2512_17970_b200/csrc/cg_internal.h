@@ -124,6 +124,10 @@ constexpr int kFlagDeterministic = 16;  // split-K by tickets + ordered sums (el
 constexpr int kFlagXRegs = 32;  // x staged through registers (unaligned x / odd cols / n > 1)
 constexpr int kFlagXcLL = 128;  // exchange launch: LL stage pushes (GroupParams::xc_ll)
 constexpr int kFlagLLChain = 1 << 16;  // staged launch: LL partials between stages, no barriers
+// contiguous task ranges: CTA c runs a stage's tasks [c*T/G, (c+1)*T/G) (not c, c+G, ...),
+// so its consecutive tasks mostly share a (layer, K-slice) and reuse that slice's
+// Psumbook without a rebuild (reduce-add split-K only; the host sets it)
+constexpr int kFlagContig = 1 << 17;
 // diagnostics only (CG_DEBUG_FLAGS): wrong results, phase isolation for timing
 constexpr int kFlagRowDeps = 64;  // stages ordered by row-group readiness, not grid barriers
 constexpr int kFlagDirectAdd = 1 << 14;  // split-K partials red.add'ed into y even at n == 1

@@ -1276,11 +1276,40 @@ __device__ __forceinline__ bool locate_s(const CtaState& cs, int nl, int s, int6
     c.g = g;
     return true;
 }
-__device__ __forceinline__ bool next_task_s(const CtaState& cs, int nl, int ns, TaskCoord& c) {
+// the stage-wide task numbers of stage s this CTA runs: g0, g0 + step, ... below
+// g_end.  Strided (c, c + G, ...) or, with kFlagContig and more tasks than CTAs,
+// one contiguous range [c*T/G, (c+1)*T/G): tasks are numbered (layer, slice,
+// row block) with the row block fastest, so a range crosses few K-slices.
+__device__ __forceinline__ void stage_share(const CtaState& cs, int nl, int s, bool contig,
+                                            int64_t& g0, int64_t& step, int64_t& g_end) {
+    int64_t total = 0;
+    for (int l = 0; l < nl; ++l)
+        if (cs.l_stage[l] == s) total += cs.l_tasks[l];
+    const int64_t G = gridDim.x, c = blockIdx.x;
+    if (contig && total > G) {
+        g0 = c * total / G;
+        g_end = (c + 1) * total / G;
+        step = 1;
+    } else {
+        g0 = c;
+        g_end = total;
+        step = G;
+    }
+}
+__device__ __forceinline__ bool first_task_s(const CtaState& cs, int nl, int s, bool contig,
+                                             TaskCoord& c) {
+    int64_t g0, step, g_end;
+    stage_share(cs, nl, s, contig, g0, step, g_end);
+    return g0 < g_end && locate_s(cs, nl, s, g0, c);
+}
+__device__ __forceinline__ bool next_task_s(const CtaState& cs, int nl, int ns, bool contig,
+                                            TaskCoord& c) {
     const int s = cs.l_stage[c.l];
-    if (locate_s(cs, nl, s, c.g + gridDim.x, c)) return true;
+    int64_t g0, step, g_end;
+    stage_share(cs, nl, s, contig, g0, step, g_end);
+    if (c.g + step < g_end && locate_s(cs, nl, s, c.g + step, c)) return true;
     for (int s2 = s + 1; s2 < ns; ++s2)
-        if (locate_s(cs, nl, s2, (int64_t)blockIdx.x, c)) return true;
+        if (first_task_s(cs, nl, s2, contig, c)) return true;
     return false;
 }
 
@@ -1353,7 +1382,7 @@ template <int V, int M, int U, int KB>
 __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int buf, bool first_task,
                                          bool has_next, bool x_next, TaskCoord nc,
                                          unsigned char* smem_raw, int tid, int task_idx,
-                                         bool zero_todo) {
+                                         bool zero_todo, int& prev_l, int& prev_slice) {
     using S = FusedShape<V, M, U, KB>;
     constexpr int D = S::kDepth;
     const int l = c.l;
@@ -1376,6 +1405,11 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     const int n_gs = L.n_gs;
     const uint8_t* tiles = L.codes + (int64_t)slice * L.n_rg * (int64_t)S::kTileBytes;
     const bool split = L.n_slices > 1;
+    // the previous task of this CTA built this (layer, K-slice)'s Psumbook: the
+    // table in shared memory is still valid (one column; nothing else writes it)
+    const bool reuse = (p.flags & kFlagContig) && n == 1 && l == prev_l && slice == prev_slice;
+    prev_l = l;
+    prev_slice = slice;
     CG_STAMP(0)
 
     // 1. this warp's first D code tiles into registers: they travel (from L2,
@@ -1390,7 +1424,7 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
         if (d < my_rgs) load_tile<V, M, U, KB>(tb[d], cptr + d * kStep);
     CG_FST(3)
     if (tid == 0) signal_rows(p, cs);  // the previous task, if a producer
-    if (L.dep >= 0) {
+    if (L.dep >= 0 && !reuse) {
         // x is an earlier stage's y: wait for the row groups this slice reads
         if (warp == 0) {
             const LayerTask& P = p.layer[L.dep];
@@ -1402,7 +1436,8 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
         __syncthreads();
     }
     uint16_t xreg[S::kXPerThread];
-    if (L.llx >= 0)
+    if (reuse) {
+    } else if (L.llx >= 0)
         load_x_llc<V, M, U, KB>(xreg, L, p.layer[L.llx], (unsigned)(cs.l_gen[L.llx] + 1),
                                 L.llw && g.rb == 0, slice, tid);
     else if (L.xll) load_x_ll<V, M, U, KB>(xreg, L, p, (unsigned)(cs.xc_base + 1), slice, n, 0, tid);
@@ -1445,7 +1480,9 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
             if (L.xll) load_x_ll<V, M, U, KB>(xreg, L, p, (unsigned)(cs.xc_base + 1), slice, n, col, tid);
             else load_x<V, M, U, KB>(xreg, L, slice, n, col, tid);
         }
-        if (x_by_copy(p, L)) {
+        if (reuse) {
+            // (no x, no build: the table of the previous task is this task's)
+        } else if (x_by_copy(p, L)) {
             const int64_t e0 = (int64_t)slice * (S::kSliceSegs * V);
             const int valid = (int)min((int64_t)(S::kSliceSegs * V), L.cols - e0);
             if (L.x32)
@@ -1456,15 +1493,17 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
         } else {
             store_x<V, M, U, KB>(xs, xreg, tid);
         }
-        __syncthreads();
-        if (col == 0) CG_STAMP(5)
-        if (!(p.flags & kFlagDbgSkipBuild))
-            build_psumbook_smem<V, M, U, KB>(psum, raw, xs,
-                                             L.kcount, tid);
+        if (!reuse) {
+            __syncthreads();
+            if (col == 0) CG_STAMP(5)
+            if (!(p.flags & kFlagDbgSkipBuild))
+                build_psumbook_smem<V, M, U, KB>(psum, raw, xs,
+                                                 L.kcount, tid);
 #ifdef CG_FINE_STAMPS
-        if (p.stamps && lane == 0 && task_idx == 1) p.stamps[blockIdx.x * 128 + 96 + warp] = gtimer();
+            if (p.stamps && lane == 0 && task_idx == 1) p.stamps[blockIdx.x * 128 + 96 + warp] = gtimer();
 #endif
-        __syncthreads();
+            __syncthreads();
+        }
         if (col == 0) CG_STAMP(6)
         if (col == 0 && first_task) pdl_launch_dependents();
         if (col == 0 && zero_todo) zero_arrive(p, tid);
@@ -1819,16 +1858,16 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
 // this CTA's task list (warp 1, once per launch, beside thread 0's input
 // issue): lane s counts the CTA's tasks in stage s (c, c + grid, ... below the
 // stage's task total), a prefix scan places the stages in the list, and each
-// lane locates list entries k = lane, lane + 32, ...  `scratch` is 64 ints of
+// lane locates list entries k = lane, lane + 32, ...  `scratch` is 128 ints of
 // shared memory that no task uses yet.
 __device__ __forceinline__ void enumerate_tasks(int n_layers, int n_stages, CtaState& cs,
-                                                int* scratch, int lane) {
-    const int G = gridDim.x, c = blockIdx.x;
-    int total_s = 0;
-    if (lane < n_stages)
-        for (int l = 0; l < n_layers; ++l)
-            if (cs.l_stage[l] == lane) total_s += cs.l_tasks[l];
-    const int cnt = (lane < n_stages && c < total_s) ? (total_s - c + G - 1) / G : 0;
+                                                int* scratch, int lane, bool contig) {
+    int cnt = 0;
+    int64_t g0 = 0, step = 1, g_end = 0;
+    if (lane < n_stages) {
+        stage_share(cs, n_layers, lane, contig, g0, step, g_end);
+        cnt = g0 < g_end ? (int)((g_end - g0 + step - 1) / step) : 0;
+    }
     int pre = cnt;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -1838,13 +1877,16 @@ __device__ __forceinline__ void enumerate_tasks(int n_layers, int n_stages, CtaS
     const int total = __shfl_sync(0xffffffffu, pre, 31);
     scratch[lane] = pre - cnt;  // first list slot of stage `lane` (stages <= layers <= 32)
     scratch[32 + lane] = cnt;
+    scratch[64 + lane] = (int)g0;
+    scratch[96 + lane] = (int)step;
     __syncwarp();
     const int n = min(total, kTaskList);
     for (int k = lane; k < n; k += 32) {
         int s = 0;
         while (!(k >= scratch[s] && k < scratch[s] + scratch[32 + s])) ++s;
         TaskCoord e;
-        locate_s(cs, n_layers, s, (int64_t)c + (int64_t)(k - scratch[s]) * G, e);
+        locate_s(cs, n_layers, s, (int64_t)scratch[64 + s] + (int64_t)(k - scratch[s]) * scratch[96 + s],
+                 e);
         cs.tl_l[k] = e.l;
         cs.tl_t[k] = e.t;
         cs.tl_g[k] = (int)e.g;
@@ -1893,7 +1935,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 88] = gtimer();
     TaskCoord c{0, 0, 0};
     bool have = false;
-    for (int s = 0; s < p.n_stages && !have; ++s) have = locate_s(cs, p.n_layers, s, blockIdx.x, c);
+    const bool contig = (p.flags & kFlagContig) != 0;
+    for (int s = 0; s < p.n_stages && !have; ++s) have = first_task_s(cs, p.n_layers, s, contig, c);
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 89] = gtimer();
     if (tid == 0) {
         mbar_init(&cs.in_bar[0], 1);
@@ -1913,7 +1956,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (tid >= 32 && tid < 64) {
         enumerate_tasks(p.n_layers, p.n_stages, cs, reinterpret_cast<int*>(smem_raw + p.off_list),
-                        tid & 31);
+                        tid & 31, contig);
         if (p.stamps && tid == 32) p.stamps[blockIdx.x * 128 + 91] = gtimer();
     }
     // every layer's x (and y, for write-after-read) belongs to earlier work
@@ -1970,6 +2013,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool zero_todo = cs.zero_pending != 0;  // (same in every thread)
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 125] = gtimer();
     int buf = 0, task_idx = 0;
+    int prev_l = -1, prev_slice = -1;  // (layer, K-slice) of the table in shared memory
     bool first = true;
     while (true) {
         CG_FST(0)
@@ -1997,12 +2041,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else if (cs.n_tl <= kTaskList && task_idx + 1 >= cs.n_tl) {
             has_next = false;
         } else {
-            has_next = next_task_s(cs, p.n_layers, p.n_stages, nc);  // beyond the list (rare)
+            has_next = next_task_s(cs, p.n_layers, p.n_stages, contig, nc);  // beyond the list (rare)
         }
         const bool x_next = has_next && cs.l_stage[nc.l] == stage;
         CG_FST(2)
         run_task<V, M, U, KB>(p, c, buf, first, has_next, x_next, nc, smem_raw, tid, task_idx++,
-                              zero_todo);
+                              zero_todo, prev_l, prev_slice);
         zero_todo = false;
         first = false;
         buf ^= 1;

@@ -354,6 +354,34 @@ def test_staged_block_vs_c_oracle():
         assert_within_tolerance(got[i], ref, f"block stage layer {i}")
 
 
+@pytest.mark.parametrize("contig", [True, False])
+def test_independent_block_one_stage_vs_c_oracle(contig, monkeypatch):
+    """The 8B block's 7 layers as independent layers in ONE stage: several tasks
+    per CTA, so with contiguous task ranges (default) consecutive tasks of a CTA
+    reuse the Psumbook of their (layer, K-slice) without a rebuild.  Every layer
+    against the C oracle; the strided schedule (CG_NO_CONTIG) gives the same
+    rows up to the split-K reduce-add order."""
+    if not contig:
+        monkeypatch.setenv("CG_NO_CONTIG", "1")
+    cfg = cg.QuantConfig(v=4, m=1, b=8, g=128)
+    shapes = [(4096, 4096)] * 4 + [(14336, 4096)] * 2 + [(4096, 14336)]
+    qs = [cg.random_layer(r, c, cfg, seed=900 + i) for i, (r, c) in enumerate(shapes)]
+    layers = [cg.DeviceLayer(q, u=4) for q in qs]
+    xs16 = [orc.bench_input_array(c, 1, 40 + i) for i, (r, c) in enumerate(shapes)]
+    ys = [torch.empty((r, 1), dtype=torch.float32, device="cuda") for r, _ in shapes]
+    plan = cg.StagedLaunch(layers, [cuda_x(x) for x in xs16], ys, [0] * len(shapes))
+    plan()
+    got = [y.cpu().numpy() for y in ys]
+    for i, q in enumerate(qs):
+        ref = c_oracle.codegemm([p.codes for p in q.planes], [b.entries for b in q.books],
+                                q.scales.scales, xs16[i], 4, 128, threads=8)
+        assert_within_tolerance(got[i], ref, f"independent layer {i} (contig={contig})")
+        assert orc.rel_l2(got[i], ref) <= 1e-5
+    plan()  # a second launch of the prepared plan: same rows
+    for i in range(len(shapes)):
+        assert orc.rel_l2(ys[i].cpu().numpy(), got[i]) <= 1e-6
+
+
 def test_staged_launch_rejects_unaligned_output():
     q = cg.random_layer(256, 1024, cg.QuantConfig(v=4, m=1, b=8, g=128), seed=31)
     dl = cg.DeviceLayer(q, u=2)

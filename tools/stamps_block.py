@@ -20,6 +20,7 @@ from paper_2512_17970_b200 import _lib  # noqa: E402
 from oracle import codegemm_oracle as orc  # noqa: E402
 
 chain = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+INDEP = int(os.environ.get("INDEP", "0"))  # 1: every layer independent, one stage
 XCHG = int(os.environ.get("XCHG", "0"))  # 1: through a world-1 comm, every layer pushed
 cfg = bench.CONFIGS["m1v4g128"]
 spec = bench.block_spec("8b")
@@ -46,6 +47,10 @@ for k in range(2):
             else:
                 xs.append(x0 if j == 0 else ys[(j - 1) * nl + nl - 1])
             st.append(4 * j + bench.STEP_STAGES[i])
+    if INDEP:
+        xs = [torch.from_numpy(orc.bench_input_array(c, 1, 10 * k + i)).cuda()
+              for j in range(chain) for i, (_, r, c) in enumerate(spec)]
+        st = [0] * len(layers)
     sets.append((layers, xs, ys, st, comm))
 s = torch.cuda.Stream()
 with torch.cuda.stream(s):
