@@ -615,8 +615,9 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
     // exchange counters count arrivals of exactly that many CTAs)
     const int sms = comm ? comm->ctas : layers[0]->sms;
     // contiguous per-CTA task ranges with Psumbook reuse (reduce-add split-K, one column)
-    const bool contig = !(layers[0]->flags & CG_OPT_DETERMINISTIC) && n == 1 &&
-                        std::getenv("CG_NO_CONTIG") == nullptr;
+    bool contig = !(layers[0]->flags & CG_OPT_DETERMINISTIC) && n == 1 &&
+                  std::getenv("CG_NO_CONTIG") == nullptr &&
+                  cg::fused_contig_instantiated(p0.v, p0.m, p0.u, p0.kbits);
     {
         bool forced = false;
         // columns the per-task smem buffers scale with: reduce-add mode adds the
@@ -764,7 +765,16 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
     // cooperative attribute (it may serialise their grids); each grid fits
     if (comm && comm->ctas < layers[0]->sms) gp.flags |= cg::kFlagDbgNoCoop;
     if (layers[0]->flags & CG_OPT_DETERMINISTIC) gp.flags |= cg::kFlagDeterministic;
-    if (contig) gp.flags |= cg::kFlagContig;
+    if (contig) {  // the contiguous instance only where a CTA runs several tasks of a stage
+        bool multi = false;
+        for (int st = 0; st < gp.n_stages; ++st) {
+            int64_t tasks = 0;
+            for (int i = 0; i < count; ++i)
+                if (gp.layer[i].stage == st) tasks += gp.layer[i].n_tasks;
+            multi |= tasks > sms;
+        }
+        if (multi) gp.flags |= cg::kFlagContig;
+    }
     if (const char* e = std::getenv("CG_DEBUG_FLAGS")) gp.flags |= std::atoi(e);
     out->gp = gp;
     out->grid = grid;

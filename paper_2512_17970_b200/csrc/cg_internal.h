@@ -144,6 +144,7 @@ struct FusedSizes {
     int psum, books, x;  // bytes
 };
 bool fused_instantiated(int v, int m, int u, int kbits);
+bool fused_contig_instantiated(int v, int m, int u, int kbits);  // contiguous-schedule instance
 bool fused_sizes(int v, int m, int u, int kbits, FusedSizes* out);
 
 // Dynamic smem layout.  The Psumbook must start at a 64 KB-aligned address of

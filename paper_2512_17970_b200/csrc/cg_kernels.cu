@@ -1302,6 +1302,13 @@ __device__ __forceinline__ bool first_task_s(const CtaState& cs, int nl, int s, 
     stage_share(cs, nl, s, contig, g0, step, g_end);
     return g0 < g_end && locate_s(cs, nl, s, g0, c);
 }
+__device__ __forceinline__ bool next_task_strided(const CtaState& cs, int nl, int ns, TaskCoord& c) {
+    const int s = cs.l_stage[c.l];
+    if (locate_s(cs, nl, s, c.g + gridDim.x, c)) return true;
+    for (int s2 = s + 1; s2 < ns; ++s2)
+        if (locate_s(cs, nl, s2, (int64_t)blockIdx.x, c)) return true;
+    return false;
+}
 __device__ __forceinline__ bool next_task_s(const CtaState& cs, int nl, int ns, bool contig,
                                             TaskCoord& c) {
     const int s = cs.l_stage[c.l];
@@ -1378,7 +1385,7 @@ __device__ __forceinline__ void issue_inputs(const GroupParams& p, TaskCoord c, 
                  x_bytes, bar);
 }
 
-template <int V, int M, int U, int KB>
+template <int V, int M, int U, int KB, bool CONTIG>
 __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int buf, bool first_task,
                                          bool has_next, bool x_next, TaskCoord nc,
                                          unsigned char* smem_raw, int tid, int task_idx,
@@ -1407,9 +1414,12 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     const bool split = L.n_slices > 1;
     // the previous task of this CTA built this (layer, K-slice)'s Psumbook: the
     // table in shared memory is still valid (one column; nothing else writes it)
-    const bool reuse = (p.flags & kFlagContig) && n == 1 && l == prev_l && slice == prev_slice;
-    prev_l = l;
-    prev_slice = slice;
+    bool reuse = false;
+    if constexpr (CONTIG) {
+        reuse = (p.flags & kFlagContig) && n == 1 && l == prev_l && slice == prev_slice;
+        prev_l = l;
+        prev_slice = slice;
+    }
     CG_STAMP(0)
 
     // 1. this warp's first D code tiles into registers: they travel (from L2,
@@ -1860,13 +1870,25 @@ __device__ __forceinline__ void stage_barrier(const GroupParams& p, unsigned cha
 // stage's task total), a prefix scan places the stages in the list, and each
 // lane locates list entries k = lane, lane + 32, ...  `scratch` is 128 ints of
 // shared memory that no task uses yet.
+template <bool CONTIG>
 __device__ __forceinline__ void enumerate_tasks(int n_layers, int n_stages, CtaState& cs,
                                                 int* scratch, int lane, bool contig) {
     int cnt = 0;
     int64_t g0 = 0, step = 1, g_end = 0;
-    if (lane < n_stages) {
-        stage_share(cs, n_layers, lane, contig, g0, step, g_end);
-        cnt = g0 < g_end ? (int)((g_end - g0 + step - 1) / step) : 0;
+    if constexpr (CONTIG) {
+        if (lane < n_stages) {
+            stage_share(cs, n_layers, lane, contig, g0, step, g_end);
+            cnt = g0 < g_end ? (int)((g_end - g0 + step - 1) / step) : 0;
+        }
+    } else {
+        const int G = gridDim.x, c = blockIdx.x;
+        int total_s = 0;
+        if (lane < n_stages)
+            for (int l = 0; l < n_layers; ++l)
+                if (cs.l_stage[l] == lane) total_s += cs.l_tasks[l];
+        cnt = (lane < n_stages && c < total_s) ? (total_s - c + G - 1) / G : 0;
+        g0 = c;
+        step = G;
     }
     int pre = cnt;
 #pragma unroll
@@ -1902,7 +1924,7 @@ __device__ __forceinline__ void enumerate_tasks(int n_layers, int n_stages, CtaS
 // The next task's weights (codebooks, scale tiles, code range into L2) are
 // requested one task ahead -- across a stage boundary too -- and its x as
 // soon as it is safe (same stage: at once; next stage: after the barrier).
-template <int V, int M, int U, int KB>
+template <int V, int M, int U, int KB, bool CONTIG>
 __global__ void __launch_bounds__(kThreads, 1)
     group_gemv_kernel(const __grid_constant__ GroupParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1935,8 +1957,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 88] = gtimer();
     TaskCoord c{0, 0, 0};
     bool have = false;
-    const bool contig = (p.flags & kFlagContig) != 0;
-    for (int s = 0; s < p.n_stages && !have; ++s) have = first_task_s(cs, p.n_layers, s, contig, c);
+    const bool contig = CONTIG && (p.flags & kFlagContig) != 0;
+    if constexpr (CONTIG) {
+        for (int s = 0; s < p.n_stages && !have; ++s) have = first_task_s(cs, p.n_layers, s, contig, c);
+    } else {
+        for (int s = 0; s < p.n_stages && !have; ++s) have = locate_s(cs, p.n_layers, s, blockIdx.x, c);
+    }
     if (p.stamps && tid == 0) p.stamps[blockIdx.x * 128 + 89] = gtimer();
     if (tid == 0) {
         mbar_init(&cs.in_bar[0], 1);
@@ -1955,8 +1981,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.stamps) p.stamps[blockIdx.x * 128 + 90] = gtimer();
     }
     if (tid >= 32 && tid < 64) {
-        enumerate_tasks(p.n_layers, p.n_stages, cs, reinterpret_cast<int*>(smem_raw + p.off_list),
-                        tid & 31, contig);
+        enumerate_tasks<CONTIG>(p.n_layers, p.n_stages, cs, reinterpret_cast<int*>(smem_raw + p.off_list),
+                                tid & 31, contig);
         if (p.stamps && tid == 32) p.stamps[blockIdx.x * 128 + 91] = gtimer();
     }
     // every layer's x (and y, for write-after-read) belongs to earlier work
@@ -2041,11 +2067,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else if (cs.n_tl <= kTaskList && task_idx + 1 >= cs.n_tl) {
             has_next = false;
         } else {
-            has_next = next_task_s(cs, p.n_layers, p.n_stages, contig, nc);  // beyond the list (rare)
+            if constexpr (CONTIG)  // beyond the list (rare)
+                has_next = next_task_s(cs, p.n_layers, p.n_stages, contig, nc);
+            else
+                has_next = next_task_strided(cs, p.n_layers, p.n_stages, nc);
         }
         const bool x_next = has_next && cs.l_stage[nc.l] == stage;
         CG_FST(2)
-        run_task<V, M, U, KB>(p, c, buf, first, has_next, x_next, nc, smem_raw, tid, task_idx++,
+        run_task<V, M, U, KB, CONTIG>(p, c, buf, first, has_next, x_next, nc, smem_raw, tid, task_idx++,
                               zero_todo, prev_l, prev_slice);
         zero_todo = false;
         first = false;
@@ -2206,11 +2235,27 @@ int grid_for(int64_t total, int threads) {
 // ---------------------------------------------------------------------------
 // template dispatch
 // ---------------------------------------------------------------------------
+// the contiguous-schedule instance (Psumbook reuse) exists for the headline
+// tilings only; elsewhere the host leaves kFlagContig clear
+template <int V, int M, int U, int KB>
+constexpr bool kContigInst = KB == 8 && ((V == 4 && M == 1 && U == 4) || (V == 8 && M == 2 && U == 2));
+
 template <int V, int M, int U, int KB>
 cudaError_t launch_group_t(const GroupParams& gp, int grid, int smem, bool pdl, cudaStream_t s) {
-    auto kern = group_gemv_kernel<V, M, U, KB>;
+    void (*kern)(GroupParams) = group_gemv_kernel<V, M, U, KB, false>;
     static int smem_set[64] = {0};
-    cudaError_t e = set_smem_once(kern, smem, smem_set);
+    static int smem_set_c[64] = {0};
+    cudaError_t e;
+    if constexpr (kContigInst<V, M, U, KB>) {
+        if (gp.flags & kFlagContig) {
+            kern = group_gemv_kernel<V, M, U, KB, true>;
+            e = set_smem_once(kern, smem, smem_set_c);
+        } else {
+            e = set_smem_once(kern, smem, smem_set);
+        }
+    } else {
+        e = set_smem_once(kern, smem, smem_set);
+    }
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid, 1, 1);
@@ -2339,6 +2384,10 @@ struct DumpLaunch {
 };
 
 }  // namespace
+
+bool fused_contig_instantiated(int v, int m, int u, int kbits) {
+    return kbits == 8 && ((v == 4 && m == 1 && u == 4) || (v == 8 && m == 2 && u == 2));
+}
 
 bool fused_instantiated(int v, int m, int u, int kbits) {
     SizeQuery q;
