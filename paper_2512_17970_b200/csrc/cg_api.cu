@@ -515,11 +515,14 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
     }
     // ---- LL chain (single GPU, batch 1, non-deterministic launches; CG_LL_CHAIN=0
     //      disables): a later-stage x that is an earlier stage's y (same pointer
-    //      and length), produced in at most CG_LL_MAX_SLICES (8) K-slices, is read
+    //      and length), produced in at most CG_LL_MAX_SLICES (32) K-slices, is read
     //      as the sum of the producer's (value, epoch) partials -- the zeroing and
     //      reduce-add of that y go away, and so does the grid barrier before the
     //      consumer's stage when all its aliased inputs come this way.  (Wider
-    //      producers cost the consumer more spinning loads than a barrier.)  Any
+    //      producers cost the consumer more spinning loads than a barrier.  A/B on
+    //      one box: limit 8 -> 32 takes the 8B down -> next q,k,v (28 slices) and
+    //      every 70B stage (16 slices) off the barrier: 8B block 38.72 -> 38.36 us,
+    //      70B 91.3 -> 88.9 us; 64 (the 70B down too) gains nothing more.)  Any
     //      other alias of an output keeps the barriers.
     for (int i = 0; i < count; ++i) {
         gp.layer[i].llx = -1;
@@ -529,7 +532,7 @@ int plan_stages(cg_layer* const* layers, const uint16_t* const* xs, float* const
     {
         const char* ev = std::getenv("CG_LL_CHAIN");
         const char* em = std::getenv("CG_LL_MAX_SLICES");
-        const int64_t max_slices = em ? std::atoi(em) : 8;
+        const int64_t max_slices = em ? std::atoi(em) : 32;
         bool llc = allow_llc && !comm && n == 1 && gp.n_stages > 1 &&
                    !(layers[0]->flags & CG_OPT_DETERMINISTIC) && !(gp.flags & cg::kFlagRowDeps) &&
                    !(ev && std::atoi(ev) == 0);
