@@ -606,11 +606,16 @@ def main():
         # a multiple of the copy count
         nlaunch = len(blocks) // CHAIN
         graphs = [capture(lambda: [run_staged_chain(CHAIN * k) for k in range(nlaunch)])]
+        # a step count that is not a multiple of the graph's: chained launches of
+        # CHAIN copies first (the copies after the graph's, rotating on), then
+        # single-block launches for what remains
+        pairs = [capture(lambda j0=j0: run_staged_chain(j0))
+                 for j0 in range(CHAIN * nlaunch, CHAIN * nlaunch + len(blocks), CHAIN)]
         singles = [capture(lambda b=b: run_staged(b)) for b in blocks]
         launches_per_step = 1.0 / CHAIN
     else:
         graphs = [capture(lambda b=b: run_xchg(b)) for b in blocks]
-        singles = None
+        singles = pairs = None
         launches_per_step = 1
 
     def timed(replays, count, per_graph=1):
@@ -621,10 +626,17 @@ def main():
         torch.cuda.synchronize(dev)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
+            # a ~0.1 ms spin kernel ahead of the start event (outside the timed
+            # region): the host has queued the timed graphs by the time the start
+            # event fires, so a short region does not time the host's first submit
+            torch.cuda._sleep(200_000)
             ev0.record(stream)
             for i in range(count // per_graph):
                 replays[i % len(replays)].replay()
-            for i in range(count % per_graph):  # exactly `count` steps
+            rem = count % per_graph  # exactly `count` steps
+            for i in range(rem // CHAIN):
+                pairs[i % len(pairs)].replay()
+            for i in range(rem % CHAIN):
                 singles[i].replay()
             ev1.record(stream)
         torch.cuda.synchronize(dev)
@@ -887,7 +899,8 @@ def main():
             **extras,
             "cpu_baseline": base, "cpu_baseline_c": base_c,
             "e2e": e2e,
-            "gpu_launches": (args.steps // spg * (spg // CHAIN) + args.steps % spg) if world == 1
+            "gpu_launches": (args.steps // spg * (spg // CHAIN) + (args.steps % spg) // CHAIN
+                             + (args.steps % spg) % CHAIN) if world == 1
             else launches_per_step * args.steps,
             "clocks": clocks,
         }
