@@ -1,0 +1,7 @@
+for rep in 1 2; do for e in "" "CG_DEBUG_FLAGS=1048576"; do
+  env $e timeout 600 python bench.py --no-cpu-baseline --no-extras --steps 2000 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('[$e] 8b', d['us_per_block'], d['roofline']['frac'], d['us_per_layer'])"
+done; done
+for e in "" "CG_DEBUG_FLAGS=1048576"; do
+  env $e timeout 600 python bench.py --workload 70b --no-cpu-baseline --no-extras --steps 500 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('[$e] 70b', d['us_per_block'], d['roofline']['frac'])"
+done
+CG_DEBUG_FLAGS=1048576 timeout 120 python tools/stamps_block.py 2 2>&1 | grep "task1"
