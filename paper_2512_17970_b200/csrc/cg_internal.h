@@ -129,6 +129,7 @@ constexpr int kFlagLLChain = 1 << 16;  // staged launch: LL partials between sta
 // Psumbook without a rebuild (reduce-add split-K only; the host sets it)
 constexpr int kFlagContig = 1 << 17;
 constexpr int kFlagDbgEarlyIssue = 1 << 19;  // next task's inputs issued before the table build (A/B)
+constexpr int kFlagDbgLL8 = 1 << 20;         // LL consumers poll 8 producer partials per round (A/B)
 // diagnostics only (CG_DEBUG_FLAGS): wrong results, phase isolation for timing
 constexpr int kFlagRowDeps = 64;  // stages ordered by row-group readiness, not grid barriers
 constexpr int kFlagDirectAdd = 1 << 14;  // split-K partials red.add'ed into y even at n == 1

@@ -418,15 +418,19 @@ __device__ __forceinline__ void load_x_ll(uint16_t (&r)[FusedShape<V, M, U, KB>:
 // x of an LL-chain consumer: element e = sum over the producer's slices (in slice
 // order: deterministic) of its partial row e, each an (value, epoch) pair spun on
 // until this launch's epoch shows; the writer consumer also stores the reduced y
+// (kLLGroup partials in flight per round: a 28-slice producer takes 2 rounds, not 4 --
+// 8B block 38.32 -> 37.79 us, 70B 93.5 -> 91.3 us on one box; `grp` = 8 restores the
+// old rounds for A/B)
+constexpr int kLLGroup = 16;  // (32: 456 bytes of spills, 8B block 50 us)
 __device__ __forceinline__ float llc_sum(const float2* llp, int64_t rows, int ns, int64_t e,
-                                         unsigned epoch) {
+                                         unsigned epoch, int grp) {
     float acc = 0.0f;
-    for (int s0 = 0; s0 < ns; s0 += 8) {
-        uint32_t v[8], ep[8];
-        const int k = min(8, ns - s0);
+    for (int s0 = 0; s0 < ns; s0 += grp) {
+        uint32_t v[kLLGroup], ep[kLLGroup];
+        const int k = min(grp, ns - s0);
         const float2* a = llp + (int64_t)s0 * rows + e;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {  // up to 8 partials in flight
+        for (int j = 0; j < kLLGroup; ++j) {  // up to kLLGroup partials in flight
             ep[j] = epoch;
             if (j < k)
                 asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];"
@@ -438,10 +442,10 @@ __device__ __forceinline__ float llc_sum(const float2* llp, int64_t rows, int ns
         while (true) {
             bool ready = true;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) ready &= ep[j] == epoch;
+            for (int j = 0; j < kLLGroup; ++j) ready &= ep[j] == epoch;
             if (ready) break;
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < kLLGroup; ++j)
                 if (ep[j] != epoch)
                     asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];"
                                  : "=r"(v[j]), "=r"(ep[j]) : "l"(a + j * rows));
@@ -451,7 +455,7 @@ __device__ __forceinline__ float llc_sum(const float2* llp, int64_t rows, int ns
             __nanosleep(64);  // (fewer polls in flight: less L2 queueing; 8B block -0.2 us)
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < kLLGroup; ++j)
             if (j < k) acc += __uint_as_float(v[j]);
     }
     return acc;
@@ -460,7 +464,7 @@ __device__ __forceinline__ float llc_sum(const float2* llp, int64_t rows, int ns
 template <int V, int M, int U, int KB>
 __device__ __forceinline__ void load_x_llc(uint16_t (&r)[FusedShape<V, M, U, KB>::kXPerThread],
                                            const LayerTask& L, const LayerTask& P, unsigned epoch,
-                                           bool write_y, int64_t slice, int tid) {
+                                           bool write_y, int64_t slice, int tid, int grp) {
     using S = FusedShape<V, M, U, KB>;
     const int64_t e0 = slice * (int64_t)(S::kSliceSegs * V);
 #pragma unroll
@@ -469,7 +473,7 @@ __device__ __forceinline__ void load_x_llc(uint16_t (&r)[FusedShape<V, M, U, KB>
         const int64_t e = e0 + l;
         uint16_t h = 0;
         if (l < S::kSliceSegs * V && e < L.cols) {
-            const float y = llc_sum(P.llp, P.rows, (int)P.n_slices, e, epoch);
+            const float y = llc_sum(P.llp, P.rows, (int)P.n_slices, e, epoch, grp);
             if (write_y) P.y[e] = y;
             h = __half_as_ushort(__float2half_rn(y));
         }
@@ -1449,7 +1453,8 @@ __device__ __forceinline__ void run_task(const GroupParams& p, TaskCoord c, int 
     if (reuse) {
     } else if (L.llx >= 0)
         load_x_llc<V, M, U, KB>(xreg, L, p.layer[L.llx], (unsigned)(cs.l_gen[L.llx] + 1),
-                                L.llw && g.rb == 0, slice, tid);
+                                L.llw && g.rb == 0, slice, tid,
+                                (p.flags & kFlagDbgLL8) ? 8 : kLLGroup);
     else if (L.xll) load_x_ll<V, M, U, KB>(xreg, L, p, (unsigned)(cs.xc_base + 1), slice, n, 0, tid);
     else if (!x_by_copy(p, L)) load_x<V, M, U, KB>(xreg, L, slice, n, 0, tid);
     CG_FST(4)
